@@ -1,0 +1,175 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * vsa_b200.h — C ABI of the B200-native VSA (Video Sparse Attention) hot path.
+ *
+ * Drop-in boundary for the reference's C++ entry points in
+ * /root/reference/proj/include/vsa/*.hpp. Every function takes plain device
+ * pointers and sizes (no torch / Eigen types), is stream-ordered and
+ * asynchronous, and returns an int status:
+ *     0            success
+ *     < 0          invalid argument (VSA_EINVAL) — the reference throws
+ *                  std::invalid_argument for the same preconditions
+ *                  (tensor.hpp:18-20); message via vsa_last_error()
+ *     > 0          a cudaError_t from a launch
+ * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *
+ * Tensor conventions (AttnTensor, tensor.hpp:44-123): contiguous [B, H, S, d].
+ *   raster  : S = t*h*w tokens in t-major raster order (the video grid)
+ *   tiled   : S = nc*cube tokens in cube-contiguous order (layout.hpp:43-55),
+ *             zero-padded to cube multiples when pad_mode = VSA_PAD_ZERO
+ *   cube    : S = nc, one row per cube (pooled / coarse quantities), fp32
+ * dtype VSA_BF16 = bf16 storage with fp32 accumulation (tcgen05 path);
+ * dtype VSA_F32  = fp32 storage and arithmetic (parity mode, SIMT kernels).
+ */
+#ifndef VSA_B200_H_
+#define VSA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { VSA_OK = 0, VSA_EINVAL = -1 };
+enum { VSA_F32 = 0, VSA_BF16 = 1 };
+enum { VSA_POOL_MEAN = 0, VSA_POOL_MAX = 1 };            /* PoolMode, coarse.hpp:13 */
+enum { VSA_PAD_REJECT = 0, VSA_PAD_ZERO = 1 };           /* layout.cpp:10-11 rejects; ZERO = extension */
+enum { VSA_GATE_IDENTITY = 0, VSA_GATE_SIGMOID = 1 };    /* GateActivation, vsa.hpp:9 */
+
+/* Fine-stage epilogue flags (vsa_fine_forward). */
+enum {
+  VSA_FINE_COMBINE = 1,     /* out = Oc*Gc + Of*Gf (vsa.hpp:118-120); needs gc, gf/ADAPTATION, oc_cube */
+  VSA_FINE_UNTILE = 2,      /* write `out` in raster order (layout.hpp:58-70), padded rows dropped */
+  VSA_FINE_ADAPTATION = 4,  /* Gf == 1 (vsa.hpp:112): gf may be NULL */
+  VSA_FINE_FORCE_SIMT = 8   /* use the SIMT kernels even for bf16 (debug / cross-check) */
+};
+
+/* TileLayout (layout.hpp:14-33, layout.cpp:6-31), plus padded extents. */
+typedef struct vsa_layout_t {
+  int64_t t, h, w;        /* token extents of the raster grid */
+  int64_t ct, ch, cw;     /* cube extents */
+  int64_t tp, hp, wp;     /* padded extents (== t,h,w unless padded) */
+  int64_t nt, nh, nw;     /* cubes per axis */
+  int64_t cube;           /* tokens per cube (B) */
+  int64_t seq;            /* raster tokens t*h*w (L) */
+  int64_t seq_padded;     /* nc*cube */
+  int64_t nc;             /* number of cubes */
+  int32_t pad_mode;
+  int32_t reserved;
+} vsa_layout_t;
+
+/* Last error message of the calling thread ("" if none). */
+const char* vsa_last_error(void);
+/* Library version / build string. */
+const char* vsa_version(void);
+
+/* Replaces: TileLayout::TileLayout (layout.cpp:6-31). VSA_PAD_REJECT reproduces
+ * the reference's divisibility check (layout.cpp:10-11); VSA_PAD_ZERO rounds the
+ * extents up to cube multiples. */
+int vsa_layout_make(int64_t t, int64_t h, int64_t w, int64_t ct, int64_t ch, int64_t cw, int32_t pad_mode,
+                    vsa_layout_t* out);
+
+/* Replaces: flatten_index (layout.cpp:40-42); host-side, no device work.
+ * Out-of-range coordinates -> VSA_EINVAL (raster_index, layout.cpp:33-38). */
+int vsa_flatten_index(const vsa_layout_t* layout, int64_t t, int64_t h, int64_t w, int64_t* out);
+
+/* Replaces: tile<S> / untile<S> (layout.hpp:43-70). x: raster [B*H, seq, d]
+ * <-> tiled [B*H, seq_padded, d]; padded rows are written as zeros by tile and
+ * dropped by untile. */
+int vsa_tile(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* x_raster, void* x_tiled,
+             void* stream);
+int vsa_untile(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled, void* x_raster,
+               void* stream);
+
+/* K1+K2 — Replaces: tile<S> (layout.hpp:43-55) fused with pool_cubes
+ * (coarse.hpp:47-65) for n tensors in one pass. pooled[i]: fp32 [B*H, nc, d],
+ * mean = sequential fp32 sum over the cube's tokens in tile order / cube.
+ * x_tiled[i] may be NULL (pool only). */
+int vsa_tile_pool(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, int32_t n,
+                  const void* const* x_raster, void* const* x_tiled, float* const* pooled, int32_t pool_mode,
+                  void* stream);
+/* Replaces: pool_cubes (coarse.hpp:47-65) on an already tile-ordered tensor. */
+int vsa_pool_tiled(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled,
+                   float* pooled, int32_t pool_mode, void* stream);
+
+/* K3 — Replaces: coarse_forward_select (coarse.hpp:71-117) from pooled inputs.
+ * Canonical fp32 order (bit-exact with oracle/): scores = fma-chain dot * fl(1/sqrt(d)),
+ * softmax with canon_exp and sequential row sum, top-k (ties -> lower index,
+ * ascending), Oc = Ac * Vc. Outputs: ac fp32 [B*H, nc, nc] (probabilities),
+ * oc_cube fp32 [B*H, nc, d], sel int32 [B*H, nc, top_k], and the transposed
+ * block map in CSR form (the reference's `rev`, fine.hpp:163-170):
+ * selT_offs int32 [B*H, nc+1], selT_idx int32 [B*H, nc*top_k], q-cubes ascending.
+ * selT_* may be NULL. bitmap_ws: device scratch of vsa_coarse_bitmap_bytes() bytes. */
+int vsa_coarse_forward(const vsa_layout_t* layout, int64_t bh, int64_t d, const float* qc, const float* kc,
+                       const float* vc, int64_t top_k, float* ac, float* oc_cube, int32_t* sel, int32_t* selT_offs,
+                       int32_t* selT_idx, void* bitmap_ws, void* stream);
+size_t vsa_coarse_bitmap_bytes(const vsa_layout_t* layout, int64_t bh);
+
+/* Builds the transposed CSR map from a user-supplied block map (e.g. the
+ * sel_override of vsa.hpp:93,115, or random_selection / all_cubes). */
+int vsa_selection_transpose(const vsa_layout_t* layout, int64_t bh, const int32_t* sel, int64_t top_k,
+                            int32_t* selT_offs, int32_t* selT_idx, void* bitmap_ws, void* stream);
+
+/* Replaces: BlockSelection::validate (selection.cpp:24-37) on device. Writes 0
+ * to *err_dev if every row is strictly ascending and in [0, nc), else 1. */
+int vsa_validate_selection(const int32_t* sel, int64_t rows, int64_t top_k, int64_t nc, int32_t* err_dev,
+                           void* stream);
+
+/* K4+K5 — Replaces: fine_forward (fine.hpp:43-99) and, with
+ * VSA_FINE_COMBINE|VSA_FINE_UNTILE, the combine of vsa_forward (vsa.hpp:118-120)
+ * plus untile (layout.hpp:58-70) in the epilogue.
+ *   q,k,v   : tiled [B*H, seq_padded, d] (dtype)
+ *   sel     : int32 [B*H, nc, top_k], strictly ascending rows (validated by the caller)
+ *   o_fine  : tiled [B*H, seq_padded, d] (dtype), the fine output Of
+ *   lse     : fp32 [B*H, seq_padded], row_lse = m + log(l) (fine.hpp:94-96)
+ *   row_max : fp32 [B*H, seq_padded] or NULL (fine.hpp:93)
+ *   gc, gf  : gates, same order as `out` (raster if UNTILE else tiled), dtype
+ *   oc_cube : fp32 [B*H, nc, d] coarse output at cube level
+ *   out     : combined output (dtype) or NULL. */
+int vsa_fine_forward(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* q, const void* k,
+                     const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse, float* row_max,
+                     const void* gc, const void* gf, const float* oc_cube, int32_t flags, void* out, void* stream);
+
+/* K6a — backward prologue, the elementwise part of vsa_backward (vsa.hpp:142-150)
+ * fused with the tile of dO and the fine delta:
+ *   dof  = dO*Gf (tiled, dtype)                 dgc = dO*Oc  (same order as dout)
+ *   dgf  = dO*Of (0 in adaptation)              doc_cube = sum over each cube's tokens of dO*Gc (fp32)
+ *   delta = rowsum(dof * Of)  fp32 [B*H, seq_padded]  (== fine.hpp:142-149's sum P*dP)
+ * dout, gc, gf, dgc, dgf are raster when `raster` != 0, else tiled. dgc/dgf may be NULL. */
+int vsa_backward_prologue(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, int32_t raster,
+                          const void* dout, const void* gc, const void* gf, const float* oc_cube, const void* o_fine,
+                          int32_t adaptation, void* dof, float* delta, float* doc_cube, void* dgc, void* dgf,
+                          void* stream);
+
+/* K6d — Replaces the cube-level part of coarse_backward (coarse.hpp:143-162):
+ * from doc_cube (token dOc summed per cube) produce dqc, dkc, dvc fp32 [B*H, nc, d].
+ * scratch: fp32 [B*H, nc, nc]. */
+int vsa_coarse_backward(const vsa_layout_t* layout, int64_t bh, int64_t d, const float* qc, const float* kc,
+                        const float* vc, const float* ac, const float* doc_cube, float* dqc, float* dkc, float* dvc,
+                        float* scratch, void* stream);
+
+/* K6b+K6c — Replaces: fine_backward (fine.hpp:107-204) plus the coarse unpool
+ * (coarse.hpp:164-178, mean mode) and the grad sum of vsa_backward (vsa.hpp:182-187):
+ *   dq = dQ_fine + dqc/cube (broadcast), dk, dv likewise; dqc/dkc/dvc may be NULL.
+ *   dof, lse, delta as produced by the forward / prologue; selT_* from the
+ *   coarse stage or vsa_selection_transpose. Deterministic (no atomics): dQ per
+ *   query cube, dK/dV per key cube over the transposed map, q-cubes ascending.
+ *   Unselected key cubes get exactly zero fine gradient (test_fine.cpp:149-169).
+ * raster != 0 writes dq/dk/dv in raster order (padded rows dropped). */
+int vsa_fine_backward(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* q, const void* k,
+                      const void* v, const void* dof, const float* lse, const float* delta, const int32_t* sel,
+                      int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx, const float* dqc,
+                      const float* dkc, const float* dvc, int32_t raster, int32_t flags, void* dq, void* dk,
+                      void* dv, void* stream);
+
+/* Max-pool unpool (coarse.hpp:172-176): adds dxc[cube][j] to the first argmax
+ * token of x (tiled) per (cube, channel) into dx (raster if `raster` else tiled, dtype). */
+int vsa_unpool_max_add(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled,
+                       const float* dxc, int32_t raster, void* dx, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VSA_B200_H_ */

@@ -144,11 +144,23 @@ inline S dot(const S* a, const S* b, Index n) {
   return acc;
 }
 
-// C[m x n] = A[m x k] * B[n x k]^T  (row-major), canonical fma chains.
+// C[m x n] = A[m x k] * B[n x k]^T  (row-major), canonical fma chains: every
+// C[i][j] is fma-accumulated over k ascending from 0 — bit-identical to
+// dot(A_i, B_j), but laid out i-k-j over B^T so the j loop vectorises.
 template <typename S>
 void gemm_abt(const S* A, const S* B, S* C, Index m, Index n, Index k) {
-  for (Index i = 0; i < m; ++i)
-    for (Index j = 0; j < n; ++j) C[i * n + j] = dot(A + i * k, B + j * k, k);
+  std::vector<S> bt(static_cast<size_t>(k * n));
+  for (Index j = 0; j < n; ++j)
+    for (Index p = 0; p < k; ++p) bt[p * n + j] = B[j * k + p];
+  for (Index i = 0; i < m; ++i) {
+    S* c = C + i * n;
+    std::fill(c, c + n, S(0));
+    for (Index p = 0; p < k; ++p) {
+      const S a = A[i * k + p];
+      const S* b = bt.data() + p * n;
+      for (Index j = 0; j < n; ++j) c[j] = std::fma(a, b[j], c[j]);
+    }
+  }
 }
 // C[m x n] (+)= A[m x k] * B[k x n]; sum over k ascending per element.
 template <typename S>
@@ -250,9 +262,10 @@ void coarse_forward(const Layout& L, const S* q, const S* k, const S* v, Index B
     const S* K = kc + u * nc * d;
     const S* V = vc + u * nc * d;
     S* A = ac + u * nc * nc;
+    gemm_abt(Q, K, A, nc, nc, d);
     for (Index i = 0; i < nc; ++i) {
       S* row = A + i * nc;
-      for (Index j = 0; j < nc; ++j) row[j] = dot(Q + i * d, K + j * d, d) * scale;
+      for (Index j = 0; j < nc; ++j) row[j] = row[j] * scale;
       S m = row[0];
       for (Index j = 1; j < nc; ++j) m = std::max(m, row[j]);
       S sum = S(0);
@@ -356,10 +369,17 @@ void dense_forward(const S* q, const S* k, const S* v, Index Bt, Index H, Index 
     const S* Q = q + u * Sq * d;
     const S* K = k + u * Sq * d;
     const S* V = v + u * Sq * d;
-    std::vector<S> s(Sq);
+    std::vector<S> s(Sq), kt(Sq * d);
+    for (Index j = 0; j < Sq; ++j)
+      for (Index c = 0; c < d; ++c) kt[c * Sq + j] = K[j * d + c];
     for (Index i = 0; i < Sq; ++i) {
+      std::fill(s.begin(), s.end(), S(0));
+      for (Index c = 0; c < d; ++c) {
+        const S a = Q[i * d + c];
+        for (Index j = 0; j < Sq; ++j) s[j] = std::fma(a, kt[c * Sq + j], s[j]);
+      }
       for (Index j = 0; j < Sq; ++j) {
-        s[j] = dot(Q + i * d, K + j * d, d) * scale;
+        s[j] = s[j] * scale;
         if (m && !m[i * Sq + j]) s[j] = ninf;
       }
       S mx = s[0];

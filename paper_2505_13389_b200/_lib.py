@@ -1,0 +1,98 @@
+# SPDX-License-Identifier: Apache-2.0
+"""ctypes binding of the C ABI in include/vsa_b200.h (libvsa_b200.so).
+
+The shared library is built in-tree (``paper_2505_13389_b200/_lib``) by
+``__graft_entry__.build()`` / ``make -C paper_2505_13389_b200/csrc``. There is
+no fallback: if the library is missing, importing the kernels raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libvsa_b200.so")
+CSRC = os.path.join(_PKG, "csrc")
+
+VSA_F32, VSA_BF16 = 0, 1
+POOL_MEAN, POOL_MAX = 0, 1
+PAD_REJECT, PAD_ZERO = 0, 1
+FINE_COMBINE, FINE_UNTILE, FINE_ADAPTATION, FINE_FORCE_SIMT = 1, 2, 4, 8
+
+
+class vsa_layout_t(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("t", "h", "w", "ct", "ch", "cw", "tp", "hp", "wp", "nt", "nh", "nw",
+                                         "cube", "seq", "seq_padded", "nc")] + [("pad_mode", C.c_int32),
+                                                                                 ("reserved", C.c_int32)]
+
+
+EXPORTS = [
+    "vsa_last_error", "vsa_version", "vsa_layout_make", "vsa_flatten_index", "vsa_tile", "vsa_untile",
+    "vsa_tile_pool", "vsa_pool_tiled", "vsa_coarse_forward", "vsa_coarse_bitmap_bytes", "vsa_selection_transpose",
+    "vsa_validate_selection", "vsa_fine_forward", "vsa_backward_prologue", "vsa_coarse_backward",
+    "vsa_fine_backward", "vsa_unpool_max_add",
+]
+
+
+def build(jobs: int = 8) -> str:
+    subprocess.run(["make", "-s", "-j", str(jobs), "-C", CSRC], check=True)
+    return LIB_PATH
+
+
+class VsaError(RuntimeError):
+    pass
+
+
+_lib = None
+
+P = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int32
+LP = C.POINTER(vsa_layout_t)
+
+
+def lib():
+    """Load libvsa_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libvsa_b200.so not built at {LIB_PATH}; run __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    L.vsa_last_error.restype = C.c_char_p
+    L.vsa_version.restype = C.c_char_p
+    sig = {
+        "vsa_layout_make": [I64] * 6 + [I32, LP],
+        "vsa_flatten_index": [LP, I64, I64, I64, C.POINTER(I64)],
+        "vsa_tile": [LP, I64, I64, I32, P, P, P],
+        "vsa_untile": [LP, I64, I64, I32, P, P, P],
+        "vsa_tile_pool": [LP, I64, I64, I32, I32, C.POINTER(P), C.POINTER(P), C.POINTER(P), I32, P],
+        "vsa_pool_tiled": [LP, I64, I64, I32, P, P, I32, P],
+        "vsa_coarse_forward": [LP, I64, I64, P, P, P, I64, P, P, P, P, P, P, P],
+        "vsa_selection_transpose": [LP, I64, P, I64, P, P, P, P],
+        "vsa_validate_selection": [P, I64, I64, I64, P, P],
+        "vsa_fine_forward": [LP, I64, I64, I32, P, P, P, P, I64, P, P, P, P, P, P, I32, P, P],
+        "vsa_backward_prologue": [LP, I64, I64, I32, I32, P, P, P, P, P, I32, P, P, P, P, P, P],
+        "vsa_coarse_backward": [LP, I64, I64, P, P, P, P, P, P, P, P, P, P],
+        "vsa_fine_backward": [LP, I64, I64, I32, P, P, P, P, P, P, P, I64, P, P, P, P, P, I32, I32, P, P, P, P],
+        "vsa_unpool_max_add": [LP, I64, I64, I32, P, P, I32, P, P],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = C.c_int
+    L.vsa_coarse_bitmap_bytes.argtypes = [LP, I64]
+    L.vsa_coarse_bitmap_bytes.restype = C.c_size_t
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    """Map a C-ABI status to the reference's error behaviour (invalid_argument -> ValueError)."""
+    if rc == 0:
+        return
+    msg = lib().vsa_last_error().decode()
+    if rc < 0:
+        raise ValueError(msg)
+    raise VsaError(f"CUDA error {rc}: {msg}")

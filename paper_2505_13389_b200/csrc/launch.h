@@ -1,0 +1,59 @@
+// SPDX-License-Identifier: Apache-2.0
+// Internal launchers (one per kernel family); the C ABI in capi.cu validates
+// arguments and dispatches here.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "vsa_b200.h"
+
+namespace vsa_host {
+
+int launch_tile_pool(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, int32_t n, const void* const* xr,
+                     void* const* xt, float* const* pooled, int32_t pool_mode, int in_tiled, cudaStream_t st);
+int launch_untile(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, const void* xt, void* x,
+                  cudaStream_t st);
+
+int launch_coarse_forward(const vsa_layout_t& L, int64_t bh, int64_t d, const float* qc, const float* kc,
+                          const float* vc, int64_t top_k, float* ac, float* oc_cube, int32_t* sel,
+                          int32_t* selT_offs, int32_t* selT_idx, void* bitmap, cudaStream_t st);
+int launch_selection_transpose(const vsa_layout_t& L, int64_t bh, const int32_t* sel, int64_t top_k,
+                               int32_t* selT_offs, int32_t* selT_idx, void* bitmap, cudaStream_t st);
+int launch_validate_selection(const int32_t* sel, int64_t rows, int64_t top_k, int64_t nc, int32_t* err,
+                              cudaStream_t st);
+size_t coarse_bitmap_bytes(const vsa_layout_t& L, int64_t bh);
+
+int launch_backward_prologue(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, int32_t raster,
+                             const void* dout, const void* gc, const void* gf, const float* oc_cube,
+                             const void* o_fine, int32_t adaptation, void* dof, float* delta, float* doc_cube,
+                             void* dgc, void* dgf, cudaStream_t st);
+int launch_coarse_backward(const vsa_layout_t& L, int64_t bh, int64_t d, const float* qc, const float* kc,
+                           const float* vc, const float* ac, const float* doc_cube, float* dqc, float* dkc,
+                           float* dvc, float* scratch, cudaStream_t st);
+int launch_unpool_max_add(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled,
+                          const float* dxc, int32_t raster, void* dx, cudaStream_t st);
+
+// SIMT kernels (fp32 parity mode; any cube size <= 128, d <= 128)
+int launch_fine_forward_simt(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, const void* q,
+                             const void* k, const void* v, const int32_t* sel, int64_t top_k, void* o_fine,
+                             float* lse, float* row_max, const void* gc, const void* gf, const float* oc_cube,
+                             int32_t flags, void* out, cudaStream_t st);
+int launch_fine_backward_simt(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, const void* q,
+                              const void* k, const void* v, const void* dof, const float* lse, const float* delta,
+                              const int32_t* sel, int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx,
+                              const float* dqc, const float* dkc, const float* dvc, int32_t raster, void* dq,
+                              void* dk, void* dv, cudaStream_t st);
+
+// tcgen05 kernels (bf16, cube = 64, d in {64, 128}); return 1 if the shape is unsupported
+bool sm100_fine_supported(const vsa_layout_t& L, int64_t d, int32_t dtype);
+int launch_fine_forward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, const void* q, const void* k,
+                              const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse,
+                              float* row_max, const void* gc, const void* gf, const float* oc_cube, int32_t flags,
+                              void* out, cudaStream_t st);
+int launch_fine_backward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, const void* q, const void* k,
+                               const void* v, const void* dof, const float* lse, const float* delta,
+                               const int32_t* sel, int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx,
+                               const float* dqc, const float* dkc, const float* dvc, int32_t raster, void* dq,
+                               void* dk, void* dv, cudaStream_t st);
+
+}  // namespace vsa_host

@@ -1,0 +1,151 @@
+// SPDX-License-Identifier: Apache-2.0
+// K1+K2: cube tiling fused with cube pooling.
+//
+// Replaces tile<S> (layout.hpp:43-55) and pool_cubes (coarse.hpp:47-65). One
+// HBM pass: each thread owns a 16-byte channel chunk of one cube and walks the
+// cube's tokens in tile order (closed-form coordinates, no permutation table),
+// loading raster rows with 128-bit loads, storing the tiled row with 128-bit
+// stores (zeros for padded tokens) and accumulating the pooled value in fp32
+// sequentially in tile order — the canonical order of oracle/vsa_oracle.cpp, so
+// pooled values (and everything the coarse stage derives from them) are
+// bit-exact with the oracle. HBM-bound: algorithmic bytes per tensor =
+// read bh*seq*d*es + write bh*seqp*d*es + write bh*nc*d*4.
+#include "common.cuh"
+#include "launch.h"
+
+namespace vsa_dev {
+
+template <typename T>
+struct TilePoolArgs {
+  const T* x[3];
+  T* xt[3];
+  float* pooled[3];
+};
+
+// grid.x: groups of `cpb` cubes over bh*nc, grid.y: tensor index.
+// in_tiled: input already tile-ordered (pool only).
+template <typename T>
+__global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh, int d, TilePoolArgs<T> a,
+                                                        int pool_mode, int in_tiled) {
+  constexpr int V = Vec<T>::N;
+  const int chunks = d / V;
+  const int cpb = blockDim.x / chunks;
+  const int local = threadIdx.x / chunks;
+  const int ch = threadIdx.x - local * chunks;
+  if (local >= cpb) return;
+  const int64_t g = int64_t(blockIdx.x) * cpb + local;
+  if (g >= bh * L.nc) return;
+  const int tsr = blockIdx.y;
+  const int64_t u = g / L.nc;
+  const int c = int(g - u * L.nc);
+  const T* __restrict__ x = a.x[tsr];
+  T* __restrict__ xt = a.xt[tsr];
+  float* __restrict__ pooled = a.pooled[tsr];
+
+  const int plane = L.nh * L.nw;
+  const int ci = c / plane, rem = c - ci * plane, cj = rem / L.nw, ck = rem - cj * L.nw;
+  const int t0 = ci * L.ct, h0 = cj * L.ch, w0 = ck * L.cw;
+
+  float acc[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) acc[i] = 0.f;
+  const int64_t tile_base = u * L.seqp + int64_t(c) * L.cube;
+  int o = 0;
+  for (int oi = 0; oi < L.ct; ++oi)
+    for (int oj = 0; oj < L.ch; ++oj)
+#pragma unroll 4
+      for (int ok = 0; ok < L.cw; ++ok, ++o) {
+        const int t = t0 + oi, h = h0 + oj, w = w0 + ok;
+        float v[V];
+        const bool valid = in_tiled || (t < L.t && h < L.h && w < L.w);
+        if (valid) {
+          const int64_t row = in_tiled ? tile_base + o : u * L.seq + (int64_t(t) * L.h + h) * L.w + w;
+          load16(x + row * d + ch * V, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) v[i] = 0.f;
+        }
+        if (xt) store16(xt + (tile_base + o) * d + ch * V, v);
+        if (pool_mode == VSA_POOL_MEAN) {
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] = acc[i] + v[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] = (o == 0) ? v[i] : fmaxf_ordered(acc[i], v[i]);
+        }
+      }
+  if (pooled) {
+    if (pool_mode == VSA_POOL_MEAN) {
+      const float inv = float(L.cube);
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] = acc[i] / inv;
+    }
+    float* dst = pooled + (u * L.nc + c) * d + ch * V;
+#pragma unroll
+    for (int i = 0; i < V; ++i) dst[i] = acc[i];
+  }
+}
+
+// untile: tiled -> raster row copy, padded rows dropped. One thread per 16 B chunk.
+template <typename T>
+__global__ void untile_kernel(DevLayout L, int64_t bh, int d, const T* __restrict__ xt, T* __restrict__ x) {
+  constexpr int V = Vec<T>::N;
+  const int chunks = d / V;
+  const int64_t total = bh * L.seqp * chunks;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int ch = int(i % chunks);
+    const int64_t rowt = i / chunks;
+    const int64_t u = rowt / L.seqp, pos = rowt - u * L.seqp;
+    const int64_t r = raster_of_tile(L, pos);
+    if (r < 0) continue;
+    *reinterpret_cast<uint4*>(x + (u * L.seq + r) * d + ch * V) =
+        *reinterpret_cast<const uint4*>(xt + rowt * d + ch * V);
+  }
+}
+
+}  // namespace vsa_dev
+
+namespace vsa_host {
+using namespace vsa_dev;
+
+template <typename T>
+static int launch_tile_pool_t(const vsa_layout_t& Lh, int64_t bh, int64_t d, int32_t n, const void* const* xr,
+                              void* const* xt, float* const* pooled, int32_t pool_mode, int in_tiled,
+                              cudaStream_t st) {
+  TilePoolArgs<T> a{};
+  for (int i = 0; i < n; ++i) {
+    a.x[i] = static_cast<const T*>(xr[i]);
+    a.xt[i] = xt ? static_cast<T*>(xt[i]) : nullptr;
+    a.pooled[i] = pooled ? pooled[i] : nullptr;
+  }
+  const int V = Vec<T>::N;
+  const int chunks = int(d) / V;
+  const int cpb = 128 / chunks;
+  const int64_t groups = (bh * Lh.nc + cpb - 1) / cpb;
+  dim3 grid{unsigned(groups), unsigned(n), 1u};
+  tile_pool_kernel<T><<<grid, cpb * chunks, 0, st>>>(to_dev(Lh), bh, int(d), a, pool_mode, in_tiled);
+  VSA_LAUNCH_CHECK("tile_pool_kernel");
+}
+
+int launch_tile_pool(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, int32_t n, const void* const* xr,
+                     void* const* xt, float* const* pooled, int32_t pool_mode, int in_tiled, cudaStream_t st) {
+  if (dtype == VSA_BF16)
+    return launch_tile_pool_t<__nv_bfloat16>(L, bh, d, n, xr, xt, pooled, pool_mode, in_tiled, st);
+  return launch_tile_pool_t<float>(L, bh, d, n, xr, xt, pooled, pool_mode, in_tiled, st);
+}
+
+int launch_untile(const vsa_layout_t& Lh, int64_t bh, int64_t d, int32_t dtype, const void* xt, void* x,
+                  cudaStream_t st) {
+  const int64_t total = bh * Lh.seq_padded * (d * (dtype == VSA_BF16 ? 2 : 4) / 16);
+  const int blocks = int(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  if (dtype == VSA_BF16)
+    untile_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(to_dev(Lh), bh, int(d),
+                                                         static_cast<const __nv_bfloat16*>(xt),
+                                                         static_cast<__nv_bfloat16*>(x));
+  else
+    untile_kernel<float><<<blocks, 256, 0, st>>>(to_dev(Lh), bh, int(d), static_cast<const float*>(xt),
+                                                 static_cast<float*>(x));
+  VSA_LAUNCH_CHECK("untile_kernel");
+}
+
+}  // namespace vsa_host

@@ -1,0 +1,207 @@
+# SPDX-License-Identifier: Apache-2.0
+"""GPU parity: the CUDA path through the C ABI (libvsa_b200.so) against the
+oracle on the same seeded inputs. Bit-exact for tiling / pooling / the
+fp32-coarse block map; north_star tolerances for outputs and gradients."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from gpu_helpers import Problem, assert_close, host, rounded, to_dev
+
+pytestmark = pytest.mark.gpu
+
+TINY = dict(grid=(8, 16, 16), B=1, H=2, d=64, top_k=4)           # BASELINE configs[0]
+PADDED = dict(grid=(9, 14, 22), B=2, H=2, d=64, top_k=6)          # non-divisible grid
+D128 = dict(grid=(16, 16, 16), B=1, H=2, d=128, top_k=8)
+DTYPES = [torch.float32, torch.bfloat16]
+
+
+@pytest.fixture(scope="module")
+def vsa():
+    import paper_2505_13389_b200 as v
+
+    v.lib()
+    return v
+
+
+def layout_of(vsa, p):
+    return vsa.TileLayout(*p.grid, *p.cube, pad=True)
+
+
+@pytest.mark.parametrize("cfg", [TINY, PADDED, D128], ids=["tiny", "padded", "d128"])
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
+def test_tile_pool_bitexact(vsa, cfg, dtype):
+    p = Problem(**cfg, seed=11)
+    L = layout_of(vsa, p)
+    xs = [to_dev(x, dtype) for x in (p.q, p.k, p.v)]
+    tiled, pooled = vsa.tile_pool(L, xs)
+    for x, t, pl in zip((p.q, p.k, p.v), tiled, pooled):
+        ref_t = p.pad_tile(rounded(x, dtype))
+        np.testing.assert_array_equal(host(t), ref_t)
+        np.testing.assert_array_equal(pl.cpu().numpy(), orc.pool_cubes(p.olayout, ref_t))
+        np.testing.assert_array_equal(host(vsa.untile(L, t)), rounded(x, dtype))
+    # max pooling
+    _, pooled_max = vsa.tile_pool(L, xs[:1], vsa.POOL_MAX, want_tiled=False)
+    np.testing.assert_array_equal(pooled_max[0].cpu().numpy(),
+                                  orc.pool_cubes(p.olayout, p.pad_tile(rounded(p.q, dtype)), orc.KMAX))
+
+
+def test_flatten_index_matches_oracle(vsa):
+    L = vsa.TileLayout(4, 4, 4, 2, 2, 2)
+    assert (vsa.flatten_index(L, 0, 0, 0), vsa.flatten_index(L, 1, 1, 1), vsa.flatten_index(L, 2, 0, 0)) == (0, 7, 32)
+    with pytest.raises(ValueError):
+        vsa.flatten_index(L, 4, 0, 0)
+    with pytest.raises(ValueError):
+        vsa.TileLayout(5, 4, 4, 2, 2, 2)
+
+
+@pytest.mark.parametrize("cfg", [TINY, PADDED, D128], ids=["tiny", "padded", "d128"])
+def test_coarse_blockmap_bitexact(vsa, cfg):
+    """fp32 coarse stage: probabilities, Oc and the Top-K block map bit-exact."""
+    p = Problem(**cfg, seed=31)
+    L = layout_of(vsa, p)
+    _, pooled = vsa.tile_pool(L, [to_dev(x, torch.float32) for x in (p.q, p.k, p.v)])
+    art = vsa.coarse_from_pooled(L, *pooled, p.top_k)
+    ref = orc.coarse_forward_select(p.olayout, p.pad_tile(p.q), p.pad_tile(p.k), p.pad_tile(p.v), p.top_k)
+    np.testing.assert_array_equal(art.ac.cpu().numpy(), ref.ac)
+    np.testing.assert_array_equal(art.sel.cpu().numpy(), ref.sel)
+    np.testing.assert_array_equal(art.oc_cube.cpu().numpy(), ref.oc_cube)
+    # transposed map == the reference's rev lists (fine.hpp:163-170)
+    offs, idx = art.selT_offs.cpu().numpy(), art.selT_idx.cpu().numpy()
+    nc, k = L.num_cubes, p.top_k
+    sel = ref.sel.reshape(-1, nc, k)
+    for u in range(sel.shape[0]):
+        rev = [[] for _ in range(nc)]
+        for qc in range(nc):
+            for kc in sel[u, qc]:
+                rev[kc].append(qc)
+        for kc in range(nc):
+            assert list(idx[u, offs[u, kc]:offs[u, kc + 1]]) == rev[kc]
+        assert offs[u, nc] == nc * k
+
+
+def test_topk_ties_lower_index(vsa):
+    """Exact ties (identical pooled keys) go to the lower index (coarse.hpp:30-42)."""
+    grid, d = (8, 16, 16), 64
+    L = vsa.TileLayout(*grid)
+    rng = orc.Rng(5)
+    qc = orc.randn(rng, 1, 1, L.num_cubes, d, np.float32)
+    kc = np.repeat(orc.randn(rng, 1, 1, 1, d, np.float32), L.num_cubes, axis=2)  # all keys equal
+    kc[0, 0, 5] *= 1.5
+    vc = orc.randn(rng, 1, 1, L.num_cubes, d, np.float32)
+    art = vsa.coarse_from_pooled(L, *(to_dev(x, torch.float32) for x in (qc, kc, vc)), 3)
+    ac = art.ac.cpu().numpy()[0, 0]
+    assert (ac == ac[:, :1]).sum() >= ac.shape[1] - 2  # rows are genuinely tied
+    ref_rows = np.stack([orc.topk_row(r, 3) for r in ac])
+    np.testing.assert_array_equal(art.sel.cpu().numpy()[0, 0], ref_rows)
+
+
+@pytest.mark.parametrize("cfg", [TINY, PADDED, D128], ids=["tiny", "padded", "d128"])
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
+def test_fine_forward_backward(vsa, cfg, dtype):
+    """fine_forward / fine_backward on tile-ordered inputs with a random block map."""
+    p = Problem(**cfg, seed=51)
+    L = layout_of(vsa, p)
+    rng = orc.Rng(52)
+    sel = orc.random_selection(p.B, p.H, L.num_cubes, p.top_k, rng)
+    q, k, v, do = (p.pad_tile(rounded(x, dtype)) for x in (p.q, p.k, p.v, p.dout))
+    fo, _, flse = orc.fine_forward(p.olayout, q, k, v, sel)
+    fdq, fdk, fdv = orc.fine_backward(p.olayout, q, k, v, sel, do, flse)
+    dq_, dk_, dv_, do_ = (to_dev(x, dtype) for x in (q, k, v, do))
+    dsel = to_dev(sel, torch.int32)
+    res = vsa.fine_forward(L, dq_, dk_, dv_, dsel)
+    assert_close(host(res.out), fo, dtype, "fine out")
+    np.testing.assert_allclose(res.row_lse.cpu().numpy().reshape(flse.shape), flse, atol=2e-3 if dtype != torch.float32 else 1e-4)
+    g = vsa.fine_backward(L, dq_, dk_, dv_, dsel, do_, res.row_lse, out=res.out)
+    for got, ref, n in zip(g, (fdq, fdk, fdv), ("dq", "dk", "dv")):
+        assert_close(host(got), ref, dtype, n)
+    # unselected key cubes: exactly zero dK/dV (test_fine.cpp:149-169)
+    used = np.zeros((p.B, p.H, L.num_cubes), bool)
+    for b in range(p.B):
+        for h in range(p.H):
+            used[b, h, np.unique(sel[b, h])] = True
+    dk_h = host(g[1]).reshape(p.B, p.H, L.num_cubes, -1)
+    assert (dk_h[~used] == 0).all()
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
+def test_dense_baseline_is_dense_attention(vsa, dtype):
+    """Full selection (BlockSelection::all_cubes) == dense attention (test_fine.cpp:21-42)."""
+    p = Problem(grid=(4, 8, 8), B=1, H=2, d=64, top_k=4, seed=53)
+    L = layout_of(vsa, p)
+    q, k, v = (p.pad_tile(rounded(x, dtype)) for x in (p.q, p.k, p.v))
+    dense, _, _ = orc.dense_forward(q, k, v)
+    res = vsa.fine_forward(L, *(to_dev(x, dtype) for x in (q, k, v)), vsa.all_cubes(p.B, p.H, L.num_cubes))
+    assert_close(host(res.out), dense, dtype, "dense")
+
+
+@pytest.mark.parametrize("cfg", [TINY, PADDED, D128], ids=["tiny", "padded", "d128"])
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
+def test_vsa_op_end_to_end(vsa, cfg, dtype):
+    """The full operator, raster in / raster out: forward, block map, backward incl. gate grads."""
+    p = Problem(**cfg, seed=71)
+    L = layout_of(vsa, p)
+    op = vsa.VsaOp(L, p.B, p.H, p.d, p.top_k, dtype=dtype)
+    ins = [to_dev(x, dtype) for x in (p.q, p.k, p.v, p.gc, p.gf)]
+    out = op.forward(*ins)
+    ref = p.oracle(dtype)
+    if dtype == torch.float32:
+        np.testing.assert_array_equal(op.sel.cpu().numpy(), ref["sel"])
+    else:  # bf16 inputs: the block map is bit-exact against the oracle on the same rounded inputs
+        np.testing.assert_array_equal(op.sel.cpu().numpy(), ref["sel"])
+    assert_close(host(out), ref["out"], dtype, "out")
+    dq, dk, dv, dgc, dgf = op.backward(to_dev(p.dout, dtype))
+    for got, n in ((dq, "dq"), (dk, "dk"), (dv, "dv"), (dgc, "dgc"), (dgf, "dgf")):
+        assert_close(host(got), ref[n], dtype, n)
+
+
+def test_sel_override_and_adaptation(vsa):
+    """sel_override (vsa.hpp:93,115) with adaptation (Gf == 1, k = nc): equals dense attention."""
+    p = Problem(grid=(4, 8, 8), B=1, H=2, d=64, top_k=4, seed=73)
+    L = layout_of(vsa, p)
+    dt = torch.float32
+    op = vsa.VsaOp(L, p.B, p.H, p.d, L.num_cubes, dtype=dt, adaptation=True)
+    gc0 = torch.zeros((p.B, p.H, L.seq_len, p.d), dtype=dt, device="cuda")
+    out = op.forward(*(to_dev(x, dt) for x in (p.q, p.k, p.v)), gc0, None)
+    q, k, v = (p.pad_tile(x) for x in (p.q, p.k, p.v))
+    dense, _, _ = orc.dense_forward(q, k, v)
+    assert_close(host(out), p.untile_crop(dense), dt, "adaptation == dense")
+    sel = orc.random_selection(p.B, p.H, L.num_cubes, 3, orc.Rng(74))
+    op2 = vsa.VsaOp(L, p.B, p.H, p.d, 2, dtype=dt)
+    out2 = op2.forward(*(to_dev(x, dt) for x in (p.q, p.k, p.v, p.gc, p.gf)), sel_override=to_dev(sel, torch.int32))
+    ref = p.oracle(dt, sel_override=sel, backward=False)
+    assert_close(host(out2), ref["out"], dt, "sel_override")
+
+
+def test_invalid_inputs_raise(vsa):
+    L = vsa.TileLayout(4, 8, 8)
+    q = torch.zeros((1, 1, L.seq_padded, 64), dtype=torch.bfloat16, device="cuda")
+    nc = L.num_cubes
+    for bad in (torch.tensor([[3, 1]] * nc, dtype=torch.int32), torch.tensor([[1, 1]] * nc, dtype=torch.int32),
+                torch.full((nc, 1), nc, dtype=torch.int32)):
+        with pytest.raises(ValueError):
+            vsa.fine_forward(L, q, q, q, bad.view(1, 1, nc, -1).cuda())
+    with pytest.raises(ValueError):
+        vsa.VsaOp(L, 1, 1, 64, 0)
+    with pytest.raises(ValueError):
+        vsa.VsaOp(L, 1, 1, 64, nc + 1)
+    op = vsa.VsaOp(L, 1, 1, 64, 2)
+    with pytest.raises(ValueError):
+        op.backward(torch.zeros((1, 1, L.seq_len, 64), dtype=torch.bfloat16, device="cuda"))
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
+def test_backward_deterministic(vsa, dtype):
+    p = Problem(**D128, seed=81)
+    L = layout_of(vsa, p)
+    op = vsa.VsaOp(L, p.B, p.H, p.d, p.top_k, dtype=dtype)
+    ins = [to_dev(x, dtype) for x in (p.q, p.k, p.v, p.gc, p.gf)]
+    do = to_dev(p.dout, dtype)
+    o1 = op.forward(*ins).clone()
+    g1 = [t.clone() for t in op.backward(do)]
+    o2 = op.forward(*ins)
+    g2 = op.backward(do)
+    assert torch.equal(o1, o2)
+    for a, b in zip(g1, g2):
+        assert torch.equal(a, b)
