@@ -63,6 +63,8 @@ typedef struct vsa_layout_t {
 const char* vsa_last_error(void);
 /* Library version / build string. */
 const char* vsa_version(void);
+/* Number of CUDA kernels this library has launched in this process (all entries). */
+uint64_t vsa_kernel_launches(void);
 
 /* Replaces: TileLayout::TileLayout (layout.cpp:6-31). VSA_PAD_REJECT reproduces
  * the reference's divisibility check (layout.cpp:10-11); VSA_PAD_ZERO rounds the

@@ -28,7 +28,7 @@ class vsa_layout_t(C.Structure):
 
 
 EXPORTS = [
-    "vsa_last_error", "vsa_version", "vsa_layout_make", "vsa_flatten_index", "vsa_tile", "vsa_untile",
+    "vsa_last_error", "vsa_version", "vsa_kernel_launches", "vsa_layout_make", "vsa_flatten_index", "vsa_tile", "vsa_untile",
     "vsa_tile_pool", "vsa_pool_tiled", "vsa_coarse_forward", "vsa_coarse_bitmap_bytes", "vsa_selection_transpose",
     "vsa_validate_selection", "vsa_fine_forward", "vsa_backward_prologue", "vsa_coarse_backward",
     "vsa_fine_backward", "vsa_unpool_max_add",
@@ -62,6 +62,7 @@ def lib():
     L = C.CDLL(LIB_PATH)
     L.vsa_last_error.restype = C.c_char_p
     L.vsa_version.restype = C.c_char_p
+    L.vsa_kernel_launches.restype = C.c_uint64
     sig = {
         "vsa_layout_make": [I64] * 6 + [I32, LP],
         "vsa_flatten_index": [LP, I64, I64, I64, C.POINTER(I64)],

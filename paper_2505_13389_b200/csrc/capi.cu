@@ -3,6 +3,7 @@
 // precondition messages (std::invalid_argument -> VSA_EINVAL + vsa_last_error),
 // then dispatch to the kernel launchers. No CPU compute path exists: every
 // entry either launches CUDA work or fails.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -27,6 +28,13 @@ int cuda_status(cudaError_t e, const char* where) {
   if (e == cudaSuccess) return 0;
   set_error("%s: %s", where, cudaGetErrorString(e));
   return int(e);
+}
+
+static std::atomic<uint64_t> g_launches{0};
+
+int kernel_status(const char* where) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError(), where);
 }
 
 static bool dtype_ok(int32_t dt) { return dt == VSA_F32 || dt == VSA_BF16; }
@@ -62,6 +70,7 @@ extern "C" {
 
 const char* vsa_last_error(void) { return g_err.c_str(); }
 const char* vsa_version(void) { return "vsa_b200 0.1 (sm_100a)"; }
+uint64_t vsa_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int vsa_layout_make(int64_t t, int64_t h, int64_t w, int64_t ct, int64_t ch, int64_t cw, int32_t pad_mode,
                     vsa_layout_t* out) {
@@ -232,7 +241,7 @@ int vsa_fine_backward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtyp
   VSA_REQUIRE(top_k >= 1 && top_k <= L->nc, "fine stage: selection does not match shapes");
   VSA_REQUIRE(d >= 1 && L->cube <= 128 && L->cube * d <= 8192, "fine stage: cube*head_dim > 8192 unsupported");
   cudaStream_t st = as_stream(stream);
-  if (!(flags & VSA_FINE_FORCE_SIMT) && sm100_fine_supported(*L, d, dtype))
+  if (!(flags & VSA_FINE_FORCE_SIMT) && sm100_fine_bwd_supported(*L, d, dtype))
     return launch_fine_backward_sm100(*L, bh, d, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc,
                                       dvc, raster, dq, dk, dv, st);
   return launch_fine_backward_simt(*L, bh, d, dtype, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc,

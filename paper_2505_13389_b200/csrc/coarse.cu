@@ -401,7 +401,7 @@ int launch_coarse_forward(const vsa_layout_t& L, int64_t bh, int64_t d, const fl
     cudaFuncSetAttribute(coarse_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     dim3 grid((nc + kScoreRows - 1) / kScoreRows, unsigned(bh));
     coarse_scores_kernel<<<grid, 128, smem, st>>>(nc, int(d), scale, qc, kc, ac);
-    int rc = cuda_status(cudaGetLastError(), "coarse_scores_kernel");
+    int rc = kernel_status("coarse_scores_kernel");
     if (rc) return rc;
   }
   const bool want_t = selT_offs && selT_idx;
@@ -417,7 +417,7 @@ int launch_coarse_forward(const vsa_layout_t& L, int64_t bh, int64_t d, const fl
     cudaFuncSetAttribute(coarse_softmax_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     coarse_softmax_topk_kernel<<<unsigned((rows + 3) / 4), 128, smem, st>>>(rows, nc, int(top_k), ac, sel, bitmap,
                                                                             words);
-    int rc = cuda_status(cudaGetLastError(), "coarse_softmax_topk_kernel");
+    int rc = kernel_status("coarse_softmax_topk_kernel");
     if (rc) return rc;
   }
   {
@@ -428,7 +428,7 @@ int launch_coarse_forward(const vsa_layout_t& L, int64_t bh, int64_t d, const fl
     dim3 grid((nc + R - 1) / R, unsigned(bh));
     coarse_oc_kernel<<<grid, unsigned(std::max<int64_t>(32, (d + 31) / 32 * 32)), smem, st>>>(nc, int(d), R, ac, vc,
                                                                                               oc_cube);
-    int rc = cuda_status(cudaGetLastError(), "coarse_oc_kernel");
+    int rc = kernel_status("coarse_oc_kernel");
     if (rc) return rc;
   }
   if (want_t) return build_csr(L, bh, selT_offs, selT_idx, top_k, bitmap, st);
@@ -444,7 +444,7 @@ int launch_selection_transpose(const vsa_layout_t& L, int64_t bh, const int32_t*
   const int64_t n = bh * nc * top_k;
   const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 8));
   sel_to_bitmap_kernel<<<blocks, 256, 0, st>>>(bh * nc, nc, int(top_k), sel, bitmap, words);
-  rc = cuda_status(cudaGetLastError(), "sel_to_bitmap_kernel");
+  rc = kernel_status("sel_to_bitmap_kernel");
   if (rc) return rc;
   return build_csr(L, bh, selT_offs, selT_idx, top_k, bitmap, st);
 }
@@ -465,7 +465,7 @@ int launch_coarse_backward(const vsa_layout_t& L, int64_t bh, int64_t d, const f
   const float scale = 1.0f / std::sqrt(float(d));
   dim3 grid(nc, unsigned(bh));
   coarse_bwd_ds_kernel<<<grid, 256, (d + 8) * sizeof(float), st>>>(nc, int(d), scale, ac, vc, doc_cube, scratch);
-  int rc = cuda_status(cudaGetLastError(), "coarse_bwd_ds_kernel");
+  int rc = kernel_status("coarse_bwd_ds_kernel");
   if (rc) return rc;
   coarse_bwd_grads_kernel<<<grid, unsigned((d + 31) / 32 * 32), 0, st>>>(nc, int(d), scratch, ac, qc, kc, doc_cube,
                                                                          dqc, dkc, dvc);

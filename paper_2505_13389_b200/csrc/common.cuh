@@ -98,6 +98,7 @@ __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return
 namespace vsa_host {
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
+int kernel_status(const char* where);  // counts the launch, then checks cudaGetLastError
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 }  // namespace vsa_host
 
@@ -109,4 +110,4 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
     }                                     \
   } while (0)
 
-#define VSA_LAUNCH_CHECK(where) return ::vsa_host::cuda_status(cudaGetLastError(), where)
+#define VSA_LAUNCH_CHECK(where) return ::vsa_host::kernel_status(where)

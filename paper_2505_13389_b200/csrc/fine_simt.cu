@@ -323,7 +323,7 @@ static int bwd_t(const vsa_layout_t& Lh, int64_t bh, int64_t d, const void* q, c
     fine_dq_simt_kernel<T><<<grid, kSimtThreads, smem, st>>>(
         to_dev(Lh), D, int(top_k), scale, static_cast<const T*>(q), static_cast<const T*>(k),
         static_cast<const T*>(v), static_cast<const T*>(dof), lse, delta, sel, dqc, raster, static_cast<T*>(dq));
-    int rc = cuda_status(cudaGetLastError(), "fine_dq_simt_kernel");
+    int rc = kernel_status("fine_dq_simt_kernel");
     if (rc) return rc;
   }
   {
