@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+# SPDX-License-Identifier: Apache-2.0
+"""bench.py — VSA attention forward+backward on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config wan13] [--impl ours|reference]
+
+One step = one VSA forward + backward pass (tile+pool, coarse attention + Top-K
+block map, block-sparse fine attention with gated combine + untile, backward
+prologue, coarse backward, fine dQ / dK dV) over one synthetic batch of the
+Wan2.1-1.3B 480p layer shape (BASELINE.json configs[1]): B=1, H=12, d=128,
+grid (21,30,52) zero-padded to (24,32,52), cube (4,4,4), top-k 78 of 624 cubes
+(87.5% sparsity), bf16 I/O with fp32 accumulation.
+
+value  : effective TFLOP/s = algorithmic FLOPs (fine 14*64^2*d per selected tile
+         + coarse 14*nc^2*d per (b,h)) / device time, summed
+         over ranks (weak scaling: every rank runs its own batch element),
+         inputs resident in HBM. ms_per_step is the max over ranks.
+e2e    : the same metric through the public API (VsaOp) with pinned HOST
+         buffers: H2D of q,k,v,gc,gf,dO and D2H of O,dQ,dK,dV,dGc,dGf every step.
+roofline: the dominant kernel (per-stage CUDA events on the launch stream).
+cpu_baseline: the CPU restatement (oracle/, "port") on one (b,h) head of the
+         same workload, all host threads, N=1 rank 0 only.
+Multi-GPU: torchrun, one process per GPU over NCCL (barrier + max-over-ranks
+timing only; the path has no data exchange — batch x head partitioning).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1] — the headline workload
+    "wan13": dict(workload="Wan2.1-1.3B 480p layer", grid=(21, 30, 52), B=1, H=12, d=128, top_k=78),
+    "tiny": dict(workload="tiny (configs[0] grid, d=64)", grid=(8, 16, 16), B=1, H=2, d=64, top_k=4),
+    "sweep32": dict(workload="paper sweep 32^3 d128 87.5%", grid=(32, 32, 32), B=1, H=16, d=128, top_k=64),
+    "dit": dict(workload="DiT pretraining batch", grid=(16, 32, 32), B=8, H=16, d=64, top_k=32),
+    "wan14": dict(workload="Wan2.1-14B 720p layer (1 GPU, all heads)", grid=(21, 45, 80), B=1, H=40, d=128,
+                  top_k=144),
+}
+
+STAGES = ["tile_pool", "coarse_fwd", "fine_fwd", "prologue", "coarse_bwd", "fine_bwd"]
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return dict(hbm=p["hbm_gbs"], bf16=p["bf16_tflops"], bf16_sust=p["bf16_tflops_sustained"], src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sust=1400.0, src="fallback")
+
+
+def flops(cfg, nc, top_k, d, cube=64):
+    B, H = cfg["B"], cfg["H"]
+    tiles = B * H * nc * top_k
+    fine_f = 4 * cube * cube * d * tiles
+    fine_b = 10 * cube * cube * d * tiles
+    coarse_f = 4 * nc * nc * d * B * H
+    coarse_b = 10 * nc * nc * d * B * H
+    return dict(tiles=tiles, fine_fwd=fine_f, fine_bwd=fine_b, coarse_fwd=coarse_f, coarse_bwd=coarse_b,
+                total=fine_f + fine_b + coarse_f + coarse_b)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_inputs(cfg, S, dtype, device, seed=0):
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    shape = (cfg["B"], cfg["H"], S, cfg["d"])
+    return [torch.randn(shape, generator=g, device=device, dtype=torch.float32).to(dtype) for _ in range(6)]
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_13389_b200 as vsa
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = CONFIGS[args.config]
+    dtype = torch.bfloat16
+    L = vsa.TileLayout(*cfg["grid"], pad=True)
+    nc, S, d, K = L.num_cubes, L.seq_len, cfg["d"], cfg["top_k"]
+    fl = flops(cfg, nc, K, d)
+    peaks = load_peaks()
+
+    op = vsa.VsaOp(L, cfg["B"], cfg["H"], d, K, dtype=dtype)
+    q, k, v, gc, gf, do = make_inputs(cfg, S, dtype, dev, seed=1234 + rank)
+    outs = [torch.empty_like(q) for _ in range(6)]
+
+    def step():
+        op.forward(q, k, v, gc, gf, out=outs[0], check_inputs=False)
+        op.backward(do, *outs[1:], check_inputs=False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    lib = vsa.lib()
+    n0 = lib.vsa_kernel_launches()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            step()
+        e1.record(st)
+        barrier()
+    launches = lib.vsa_kernel_launches() - n0
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    value = world * fl["total"] / (ms * 1e-3) / 1e12
+
+    # per-stage breakdown (events between stages on the launch stream)
+    stage_ms = {s: 0.0 for s in STAGES}
+    nrep = max(2, min(args.steps, 5))
+    for _ in range(nrep):
+        op.trace = []
+        step()
+        torch.cuda.synchronize()
+        tr = op.trace
+        for (_, a), (name, b) in zip(tr[:-1], tr[1:]):
+            if name in stage_ms:
+                stage_ms[name] += a.elapsed_time(b) / nrep
+    op.trace = None
+
+    # dense baseline: the same kernels with top-k = all cubes
+    dense = None
+    if not args.no_dense:
+        opd = vsa.VsaOp(L, cfg["B"], cfg["H"], d, nc, dtype=dtype)
+        fld = flops(cfg, nc, nc, d)
+
+        def dstep():
+            opd.forward(q, k, v, gc, gf, out=outs[0], check_inputs=False)
+            opd.backward(do, *outs[1:], check_inputs=False)
+
+        dstep()
+        barrier()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nd = max(1, min(args.steps, 3))
+        d0.record(st)
+        for _ in range(nd):
+            dstep()
+        d1.record(st)
+        barrier()
+        dms = max_over_ranks(d0.elapsed_time(d1) / nd)
+        dense = dict(ms_per_step=round(dms, 3), tflops=round(fld["total"] / (dms * 1e-3) / 1e12, 1),
+                     speedup_vsa_vs_dense=round(dms / ms, 2))
+        del opd
+
+    # e2e through the public API with pinned host buffers
+    hin = [t.cpu().pin_memory() for t in (q, k, v, gc, gf, do)]
+    hout = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
+    din = [torch.empty_like(t) for t in (q, k, v, gc, gf, do)]
+
+    def e2e_step():
+        for dst, src in zip(din, hin):
+            dst.copy_(src, non_blocking=True)
+        op.forward(*din[:5], out=outs[0])
+        op.backward(din[5], *outs[1:])
+        for dst, src in zip(hout, outs):
+            dst.copy_(src, non_blocking=True)
+
+    e2e_step()
+    barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    ne = max(1, min(args.steps, 5))
+    e2.record(st)
+    for _ in range(ne):
+        e2e_step()
+    e3.record(st)
+    barrier()
+    ems = max_over_ranks(e2.elapsed_time(e3) / ne)
+    h2d = sum(t.numel() * t.element_size() for t in hin)
+    d2h = sum(t.numel() * t.element_size() for t in hout)
+
+    if rank != 0:
+        return None
+
+    # roofline of the dominant kernel
+    dom = max(("fine_fwd", "fine_bwd"), key=lambda s: stage_ms[s])
+    ach = fl[dom] / (stage_ms[dom] * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            traffic = tj.get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    bytes_tp = cfg["B"] * cfg["H"] * 3 * (S * d * 2 + L.seq_padded * d * 2 + nc * d * 4)
+    stages = {}
+    for s in STAGES:
+        e = {"ms": round(stage_ms[s], 4)}
+        if s in ("fine_fwd", "fine_bwd", "coarse_fwd", "coarse_bwd") and stage_ms[s] > 0:
+            e["tflops"] = round(fl[s] / (stage_ms[s] * 1e-3) / 1e12, 1)
+        if s == "tile_pool" and stage_ms[s] > 0:
+            e["gbs"] = round(bytes_tp / (stage_ms[s] * 1e-3) / 1e9, 1)
+        stages[s] = e
+    line = {
+        "metric": "VSA fwd+bwd effective TFLOPS (algorithmic FLOPs / device time), Wan2.1-1.3B layer",
+        "value": round(value, 2),
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (torch.randn, seeded per rank)",
+        "config": {
+            "workload": cfg["workload"], "B": cfg["B"], "H": cfg["H"], "head_dim": d, "grid": list(cfg["grid"]),
+            "grid_padded": list(L.padded), "cube": [4, 4, 4], "num_cubes": nc, "top_k": K,
+            "sparsity": round(1 - K / nc, 4), "global_batch": cfg["B"] * world, "seq_len": S,
+            "parallelism": f"dp{world} (batch x head partition, no collective)",
+            "l2": "inputs larger than L2 (6 x {:.0f} MB bf16 per step)".format(q.numel() * 2 / 1e6),
+            "flops_per_step": fl["total"],
+        },
+        "frac_of_peak": round(value / world / peaks["bf16_sust"], 4),
+        "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(ach, 1), "peak": peaks["bf16_sust"],
+                     "peak_kind": f"bf16_tflops_sustained ({peaks['src']})", "unit": "TFLOP/s",
+                     "frac": round(ach / peaks["bf16_sust"], 4), "traffic": traffic,
+                     "algorithmic_flops_per_launch": fl[dom]},
+        "stages": stages,
+        "dense_baseline": dense,
+        "e2e": {"value": round(world * fl["total"] / (ems * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+                "ms_per_step": round(ems, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, 1)
+    return line
+
+
+def cpu_baseline(cfg, reps):
+    """The oracle (CPU restatement of the reference) on ONE (b,h) head of the
+    workload: coarse fwd + fine fwd + fine bwd + coarse bwd, all host threads."""
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+
+    T, X, Y = cfg["grid"]
+    Tp, Xp, Yp = orc.padded_extents(T, X, Y, 4, 4, 4)
+    L = orc.TileLayout(Tp, Xp, Yp, 4, 4, 4)
+    d, K = cfg["d"], cfg["top_k"]
+    rng = orc.Rng(0)
+    q, k, v, do = (orc.randn(rng, 1, 1, L.seq_len, d, np.float32) for _ in range(4))
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        art = orc.coarse_forward_select(L, q, k, v, K)
+        _, _, lse = orc.fine_forward(L, q, k, v, art.sel)
+        orc.fine_backward(L, q, k, v, art.sel, do, lse)
+        orc.coarse_backward(art, L, do, q, k, v)
+        times.append(time.perf_counter() - t0)
+    t = sorted(times)[len(times) // 2]
+    fl = flops(dict(B=1, H=1), L.num_cubes, K, d)["total"]
+    return {"value": round(fl / t / 1e12, 5), "unit": "TFLOP/s", "cores": orc.max_threads(), "kind": "port",
+            "sample": f"one (b,h) head of {cfg['workload']} (1/{cfg['B'] * cfg['H']} of a step), "
+                      f"coarse+fine fwd+bwd, {t:.2f} s median of {reps}", "seconds": round(t, 3)}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on the host cores (the oracle
+    port; the Eigen reference cannot be compiled here), same metric/config."""
+    if rank != 0:
+        return None
+    cfg = CONFIGS[args.config]
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+
+    orc.set_num_threads(os.cpu_count() or 1)
+    for _ in range(min(args.warmup, 1)):
+        cpu_baseline(cfg, 1)
+    cb = cpu_baseline(cfg, max(1, min(args.steps, 3)))
+    # one step of the full workload = B*H heads
+    heads = cfg["B"] * cfg["H"]
+    ms = cb["seconds"] * heads * 1e3
+    return {
+        "metric": "VSA fwd+bwd effective TFLOPS (algorithmic FLOPs / device time), Wan2.1-1.3B layer",
+        "impl": "reference", "value": cb["value"], "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (mt19937_64 randn)",
+        "config": {"workload": cfg["workload"], "B": cfg["B"], "H": cfg["H"], "head_dim": cfg["d"],
+                   "grid": list(cfg["grid"]), "top_k": cfg["top_k"],
+                   "note": "each step is a bounded sample: one (b,h) head; ms_per_step extrapolated x B*H"},
+        "cpu_baseline": {"value": cb["value"], "unit": "TFLOP/s", "cores": cb["cores"], "kind": "port",
+                         "sample": cb["sample"]},
+        "e2e": {"value": cb["value"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="wan13", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        line = run_ours(args, rank, world, local_rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

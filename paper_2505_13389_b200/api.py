@@ -361,6 +361,13 @@ class VsaOp:
         self._gc = self._gf = None
         self._lib = L.lib()
         self._lref = layout.ref()
+        self.trace = None  # optional list: (stage, torch.cuda.Event) appended after each stage
+
+    def _mark(self, name):
+        if self.trace is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.trace.append((name, ev))
 
     @property
     def seq_io(self) -> int:
@@ -388,16 +395,21 @@ class VsaOp:
             xr = (C.c_void_p * 3)(q.data_ptr(), k.data_ptr(), v.data_ptr())
             xt = (C.c_void_p * 3)(self.q_t.data_ptr(), self.k_t.data_ptr(), self.v_t.data_ptr())
             pl = (C.c_void_p * 3)(self.qc.data_ptr(), self.kc.data_ptr(), self.vc.data_ptr())
+            self._mark("start")
             check(lib.vsa_tile_pool(lr, bh, d, dt, 3, xr, xt, pl, self.pool, st))
+            self._mark("tile_pool")
             qt, kt, vt = self.q_t, self.k_t, self.v_t
         else:
             qt, kt, vt = q, k, v
+            self._mark("start")
             for x, p in ((q, self.qc), (k, self.kc), (v, self.vc)):
                 check(lib.vsa_pool_tiled(lr, bh, d, dt, _p(x), _p(p), self.pool, st))
+            self._mark("tile_pool")
         override = sel_override is not None
         check(lib.vsa_coarse_forward(lr, bh, d, _p(self.qc), _p(self.kc), _p(self.vc), self.top_k, _p(self.ac),
                                      _p(self.oc), _p(self.sel), None if override else _p(self.selT_offs),
                                      None if override else _p(self.selT_idx), _p(self.bitmap), st))
+        self._mark("coarse_fwd")
         if override:
             validate_selection(sel_override, self.layout.num_cubes)
             if sel_override.shape[:3] != self.sel.shape[:3]:
@@ -417,6 +429,7 @@ class VsaOp:
             flags |= L.FINE_FORCE_SIMT
         check(lib.vsa_fine_forward(lr, bh, d, dt, _p(qt), _p(kt), _p(vt), _p(self.fine_sel), self.fine_k,
                                    _p(self.o_f), _p(self.lse), None, _p(gc), _p(gf), _p(self.oc), flags, _p(out), st))
+        self._mark("fine_fwd")
         self._gc, self._gf = gc, gf
         self._qkv = (qt, kt, vt)
         return out
@@ -443,8 +456,10 @@ class VsaOp:
         check(lib.vsa_backward_prologue(lr, bh, d, dt, raster, _p(dout), _p(self._gc), _p(self._gf), _p(self.oc),
                                         _p(self.o_f), 1 if self.adaptation else 0, _p(self.dof), _p(self.delta),
                                         _p(self.doc), _p(dgc), _p(dgf), st))
+        self._mark("prologue")
         check(lib.vsa_coarse_backward(lr, bh, d, _p(self.qc), _p(self.kc), _p(self.vc), _p(self.ac), _p(self.doc),
                                       _p(self.dqc), _p(self.dkc), _p(self.dvc), _p(self.scratch), st))
+        self._mark("coarse_bwd")
         mean = self.pool == POOL_MEAN
         qt, kt, vt = self._qkv
         flags = L.FINE_FORCE_SIMT if self.force_simt else 0
@@ -452,6 +467,7 @@ class VsaOp:
                                     _p(self.delta), _p(self.fine_sel), self.fine_k, _p(self.selT_offs),
                                     _p(self.selT_idx), _p(self.dqc) if mean else None, _p(self.dkc) if mean else None,
                                     _p(self.dvc) if mean else None, raster, flags, _p(dq), _p(dk), _p(dv), st))
+        self._mark("fine_bwd")
         if not mean:
             for x, dc, g in ((qt, self.dqc, dq), (kt, self.dkc, dk), (vt, self.dvc, dv)):
                 check(lib.vsa_unpool_max_add(lr, bh, d, dt, _p(x), _p(dc), raster, _p(g), st))

@@ -52,47 +52,6 @@ __device__ __forceinline__ double canon_exp_d(double x) {
 }
 __device__ __forceinline__ float canon_expf(float x) { return __double2float_rn(canon_exp_d(double(x))); }
 
-// --------------------------------------------------------------------------- scores
-// grid (ceil(nc/R), bh), block 128: thread t owns key cube j = j0 + t and R query rows.
-constexpr int kScoreRows = 16;
-__global__ void __launch_bounds__(128) coarse_scores_kernel(int nc, int d, float scale, const float* __restrict__ qc,
-                                                             const float* __restrict__ kc, float* __restrict__ ac) {
-  extern __shared__ float sm[];
-  float* qs = sm;                        // [R][d]
-  float* ks = sm + kScoreRows * d;       // [128][d+1]
-  const int64_t u = blockIdx.y;
-  const int i0 = blockIdx.x * kScoreRows;
-  const int nr = min(kScoreRows, nc - i0);
-  for (int e = threadIdx.x; e < kScoreRows * d; e += blockDim.x) {
-    const int r = e / d;
-    qs[e] = r < nr ? qc[(u * nc + i0 + r) * d + (e - r * d)] : 0.f;
-  }
-  for (int j0 = 0; j0 < nc; j0 += 128) {
-    __syncthreads();
-    const int nj = min(128, nc - j0);
-    for (int e = threadIdx.x; e < nj * d; e += blockDim.x) {
-      const int r = e / d;
-      ks[r * (d + 1) + (e - r * d)] = kc[(u * nc + j0 + r) * d + (e - r * d)];
-    }
-    __syncthreads();
-    const int t = threadIdx.x;
-    if (t < nj) {
-      float acc[kScoreRows];
-#pragma unroll
-      for (int r = 0; r < kScoreRows; ++r) acc[r] = 0.f;
-      const float* kr = ks + t * (d + 1);
-      for (int c = 0; c < d; ++c) {
-        const float kv = kr[c];
-#pragma unroll
-        for (int r = 0; r < kScoreRows; ++r) acc[r] = __fmaf_rn(qs[r * d + c], kv, acc[r]);
-      }
-#pragma unroll
-      for (int r = 0; r < kScoreRows; ++r)
-        if (r < nr) ac[(u * nc + i0 + r) * int64_t(nc) + j0 + t] = __fmul_rn(acc[r], scale);
-    }
-  }
-}
-
 // --------------------------------------------------------------------------- softmax + top-k
 // One warp per (b,h,row). Dynamic smem per warp: nc floats + 256-bin histogram.
 __global__ void __launch_bounds__(128) coarse_softmax_topk_kernel(int64_t rows, int nc, int k,
@@ -200,34 +159,6 @@ __global__ void __launch_bounds__(128) coarse_softmax_topk_kernel(int64_t rows, 
   }
 }
 
-// --------------------------------------------------------------------------- Oc = Ac * Vc
-// grid (ceil(nc/R), bh), block d threads (channel); R probability rows staged in smem.
-__global__ void coarse_oc_kernel(int nc, int d, int R, const float* __restrict__ ac, const float* __restrict__ vc,
-                                 float* __restrict__ oc) {
-  extern __shared__ float ps[];  // [R][nc]
-  const int64_t u = blockIdx.y;
-  const int i0 = blockIdx.x * R;
-  const int nr = min(R, nc - i0);
-  for (int e = threadIdx.x; e < nr * nc; e += blockDim.x) ps[e] = ac[(u * nc + i0) * int64_t(nc) + e];
-  __syncthreads();
-  const int c = threadIdx.x;
-  if (c >= d) return;
-  float acc[16];
-  for (int r0 = 0; r0 < nr; r0 += 16) {
-#pragma unroll
-    for (int r = 0; r < 16; ++r) acc[r] = 0.f;
-    for (int j = 0; j < nc; ++j) {
-      const float v = vc[(u * nc + j) * d + c];
-#pragma unroll
-      for (int r = 0; r < 16; ++r)
-        if (r0 + r < nr) acc[r] = __fmaf_rn(ps[(r0 + r) * nc + j], v, acc[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r)
-      if (r0 + r < nr) oc[(u * nc + i0 + r0 + r) * d + c] = acc[r];
-  }
-}
-
 // --------------------------------------------------------------------------- transposed map
 __global__ void sel_to_bitmap_kernel(int64_t rows, int nc, int k, const int32_t* __restrict__ sel,
                                      uint32_t* __restrict__ bitmap, int words) {
@@ -295,56 +226,19 @@ __global__ void validate_sel_kernel(const int32_t* __restrict__ sel, int64_t row
 }
 
 // --------------------------------------------------------------------------- coarse backward (cube level)
-// ds = Ac .* (dP - delta) * scale,  dP = dOc Vc^T,  delta_i = sum_j Ac_ij dP_ij  (coarse.hpp:154-157)
-// grid (nc, bh), block 256: one query-cube row per block.
-__global__ void __launch_bounds__(256) coarse_bwd_ds_kernel(int nc, int d, float scale, const float* __restrict__ ac,
-                                                             const float* __restrict__ vc,
-                                                             const float* __restrict__ doc, float* __restrict__ ds) {
-  extern __shared__ float sm[];
-  float* dor = sm;            // [d]
-  float* red = sm + d;        // [8]
-  const int64_t u = blockIdx.y;
-  const int i = blockIdx.x;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) dor[c] = doc[(u * nc + i) * d + c];
-  __syncthreads();
-  const float* arow = ac + (u * nc + i) * int64_t(nc);
-  float* drow = ds + (u * nc + i) * int64_t(nc);
+// dS = Ac .* (dP - delta) * scale, delta_i = sum_j Ac_ij dP_ij (coarse.hpp:155-157). One warp per row, in place.
+__global__ void __launch_bounds__(128) coarse_bwd_ds_kernel(int64_t rows, int nc, float scale,
+                                                             const float* __restrict__ ac, float* __restrict__ ds) {
+  const int64_t row = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* a = ac + row * nc;
+  float* r = ds + row * nc;
   float part = 0.f;
-  for (int j = threadIdx.x; j < nc; j += blockDim.x) {
-    const float* vr = vc + (u * nc + j) * d;
-    float dp = 0.f;
-    for (int c = 0; c < d; ++c) dp = __fmaf_rn(dor[c], vr[c], dp);
-    drow[j] = dp;
-    part = __fmaf_rn(arow[j], dp, part);
-  }
+  for (int j = lane; j < nc; j += 32) part = __fmaf_rn(a[j], r[j], part);
 #pragma unroll
   for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
-  __syncthreads();
-  float delta = 0.f;
-  for (int w = 0; w < int(blockDim.x >> 5); ++w) delta += red[w];
-  for (int j = threadIdx.x; j < nc; j += blockDim.x) drow[j] = arow[j] * (drow[j] - delta) * scale;
-}
-
-// dqc = ds Kc, dkc = ds^T Qc, dvc = Ac^T dOc. grid (nc, bh), block d: row i, channel c.
-__global__ void coarse_bwd_grads_kernel(int nc, int d, const float* __restrict__ ds, const float* __restrict__ ac,
-                                        const float* __restrict__ qc, const float* __restrict__ kc,
-                                        const float* __restrict__ doc, float* __restrict__ dqc,
-                                        float* __restrict__ dkc, float* __restrict__ dvc) {
-  const int64_t u = blockIdx.y;
-  const int i = blockIdx.x, c = threadIdx.x;
-  if (c >= d) return;
-  const float* D = ds + u * nc * int64_t(nc);
-  const float* A = ac + u * nc * int64_t(nc);
-  float aq = 0.f, ak = 0.f, av = 0.f;
-  for (int j = 0; j < nc; ++j) {
-    aq = __fmaf_rn(D[int64_t(i) * nc + j], kc[(u * nc + j) * d + c], aq);
-    ak = __fmaf_rn(D[int64_t(j) * nc + i], qc[(u * nc + j) * d + c], ak);
-    av = __fmaf_rn(A[int64_t(j) * nc + i], doc[(u * nc + j) * d + c], av);
-  }
-  dqc[(u * nc + i) * d + c] = aq;
-  dkc[(u * nc + i) * d + c] = ak;
-  dvc[(u * nc + i) * d + c] = av;
+  for (int j = lane; j < nc; j += 32) r[j] = a[j] * (r[j] - part) * scale;
 }
 
 // max-pool unpool: route dxc to the first argmax token per (cube, channel). grid (nc, bh), block d.
@@ -397,11 +291,9 @@ int launch_coarse_forward(const vsa_layout_t& L, int64_t bh, int64_t d, const fl
   const int nc = int(L.nc);
   const float scale = 1.0f / std::sqrt(float(d));
   {
-    const size_t smem = (kScoreRows * d + 128 * (d + 1)) * sizeof(float);
-    cudaFuncSetAttribute(coarse_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    dim3 grid((nc + kScoreRows - 1) / kScoreRows, unsigned(bh));
-    coarse_scores_kernel<<<grid, 128, smem, st>>>(nc, int(d), scale, qc, kc, ac);
-    int rc = kernel_status("coarse_scores_kernel");
+    // scores = fl(Qc Kc^T) * fl(1/sqrt d)   (coarse.hpp:103-104)
+    int rc = launch_gemm_f32(int(bh), nc, nc, int(d), qc, int64_t(nc) * d, d, 1, kc, int64_t(nc) * d, 1, d, ac,
+                             int64_t(nc) * nc, nc, &scale, st);
     if (rc) return rc;
   }
   const bool want_t = selT_offs && selT_idx;
@@ -421,14 +313,9 @@ int launch_coarse_forward(const vsa_layout_t& L, int64_t bh, int64_t d, const fl
     if (rc) return rc;
   }
   {
-    int R = 16;
-    while (R > 1 && size_t(R) * nc * 4 > 160 * 1024) R /= 2;
-    const size_t smem = size_t(R) * nc * sizeof(float);
-    cudaFuncSetAttribute(coarse_oc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    dim3 grid((nc + R - 1) / R, unsigned(bh));
-    coarse_oc_kernel<<<grid, unsigned(std::max<int64_t>(32, (d + 31) / 32 * 32)), smem, st>>>(nc, int(d), R, ac, vc,
-                                                                                              oc_cube);
-    int rc = kernel_status("coarse_oc_kernel");
+    // Oc = Ac Vc (coarse.hpp:110), cube level
+    int rc = launch_gemm_f32(int(bh), nc, int(d), nc, ac, int64_t(nc) * nc, nc, 1, vc, int64_t(nc) * d, d, 1, oc_cube,
+                             int64_t(nc) * d, d, nullptr, st);
     if (rc) return rc;
   }
   if (want_t) return build_csr(L, bh, selT_offs, selT_idx, top_k, bitmap, st);
@@ -461,15 +348,22 @@ int launch_validate_selection(const int32_t* sel, int64_t rows, int64_t top_k, i
 int launch_coarse_backward(const vsa_layout_t& L, int64_t bh, int64_t d, const float* qc, const float* kc,
                            const float* vc, const float* ac, const float* doc_cube, float* dqc, float* dkc,
                            float* dvc, float* scratch, cudaStream_t st) {
-  const int nc = int(L.nc);
+  const int nc = int(L.nc), D = int(d), B = int(bh);
   const float scale = 1.0f / std::sqrt(float(d));
-  dim3 grid(nc, unsigned(bh));
-  coarse_bwd_ds_kernel<<<grid, 256, (d + 8) * sizeof(float), st>>>(nc, int(d), scale, ac, vc, doc_cube, scratch);
-  int rc = kernel_status("coarse_bwd_ds_kernel");
+  const int64_t snn = int64_t(nc) * nc, snd = int64_t(nc) * d;
+  // dP = dOc Vc^T
+  int rc = launch_gemm_f32(B, nc, nc, D, doc_cube, snd, D, 1, vc, snd, 1, D, scratch, snn, nc, nullptr, st);
   if (rc) return rc;
-  coarse_bwd_grads_kernel<<<grid, unsigned((d + 31) / 32 * 32), 0, st>>>(nc, int(d), scratch, ac, qc, kc, doc_cube,
-                                                                         dqc, dkc, dvc);
-  VSA_LAUNCH_CHECK("coarse_bwd_grads_kernel");
+  // dS = Ac .* (dP - rowsum(Ac .* dP)) * scale  (in place)
+  coarse_bwd_ds_kernel<<<unsigned((bh * nc + 3) / 4), 128, 0, st>>>(bh * nc, nc, scale, ac, scratch);
+  rc = kernel_status("coarse_bwd_ds_kernel");
+  if (rc) return rc;
+  // dQc = dS Kc, dKc = dS^T Qc, dVc = Ac^T dOc
+  rc = launch_gemm_f32(B, nc, D, nc, scratch, snn, nc, 1, kc, snd, D, 1, dqc, snd, D, nullptr, st);
+  if (rc) return rc;
+  rc = launch_gemm_f32(B, nc, D, nc, scratch, snn, 1, nc, qc, snd, D, 1, dkc, snd, D, nullptr, st);
+  if (rc) return rc;
+  return launch_gemm_f32(B, nc, D, nc, ac, snn, 1, nc, doc_cube, snd, D, 1, dvc, snd, D, nullptr, st);
 }
 
 int launch_unpool_max_add(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled,

@@ -1,20 +1,608 @@
 // SPDX-License-Identifier: Apache-2.0
-// K6b/K6c on tcgen05: placeholder dispatch (the SIMT backward runs until the
-// tcgen05 dQ and dK/dV kernels land).
+// K6b + K6c: block-sparse fine attention backward on tcgen05 / TMEM / TMA.
+//
+// Replaces fine_backward (fine.hpp:107-204), plus the mean-pool unpool of the
+// coarse path (coarse.hpp:164-168) and the grad sum of vsa_backward
+// (vsa.hpp:182-187) in the epilogues. Deterministic: no atomics anywhere.
+//
+// K6b  dQ, Q-stationary (one CTA per query cube, like fine.hpp:129-161). Keys on M
+//      (pairs of selected key cubes, as in the forward):
+//        S^T  = Kpair . Q^T,  dP^T = Vpair . dO^T               (M=128 keys, N=64 q)
+//        dS^T = P^T .* (dP^T - delta[q]),  P^T = exp2(S^T*c - lse2[q])
+//        dQ^T += Kpair^T . dS^T                                 (M=d, N=64 q, K=128 keys)
+// K6c  dK/dV, KV-stationary (one CTA per key cube, fine.hpp:172-202): pairs of the
+//      query cubes that selected it, from the transposed CSR map in ascending
+//      order — queries on M, so lse/delta are per-thread scalars:
+//        S  = Qpair . K^T,  dP = dOpair . V^T                   (M=128 q, N=64 keys)
+//        dV^T += dOpair^T . P,  dK^T += Qpair^T . dS            (M=d, N=64 keys, K=128 q)
+// The 1/sqrt(d) of dS is folded into the dQ / dK epilogues. Every A operand of a
+// transposed product is the same TMA SW128 tile read MN-major (no copies); P / dS
+// are written by the compute threads directly in the MN-major SW128 B layout.
+// Key cubes selected by no query get exactly zero fine gradient (test_fine.cpp:149-169).
+//
+// Roles (224 threads, 1 CTA/SM): warps 0-3 compute + epilogue (TMEM quadrant =
+// warp), warp 4 TMA producer A, warp 5 TMA producer B, warp 6 TMEM alloc + MMA
+// issuer. Operand stages are double-buffered; S / dP are double-buffered in TMEM
+// and the MMA issuer runs one pair ahead so the exp2 / dS math of pair p overlaps
+// the S, dP products of pair p+1.
+#include <cmath>
+
 #include "common.cuh"
 #include "launch.h"
+#include "sm100.cuh"
+#include "tmap.h"
+
+namespace vsa_dev {
+
+constexpr int kBwdThreads = 224;
+
+__device__ __forceinline__ float ex2b(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void named_bar_b(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+// [64 rows][D] fp32 staging of a TMEM [D lanes x 64 cols] accumulator (thread = lane = d row).
+template <int D>
+__device__ __forceinline__ void stage_transposed(uint32_t taddr_lane, float* st, int dl, float scale) {
+  float t[32];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    tmem_ld32(taddr_lane + h * 32, t);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) st[(h * 32 + i) * D + dl] = t[i] * scale;
+  }
+}
+
+// Write a [64][D] fp32 staged tile as bf16 rows of cube `cube`, adding xc/64 (mean unpool).
+template <int D>
+__device__ __forceinline__ void write_rows(const DevLayout& L, int64_t u, int cube, const float* st,
+                                           const float* __restrict__ xc, int raster, __nv_bfloat16* __restrict__ dst,
+                                           int tid, int nthr) {
+  constexpr int CH = D / 8;
+  const float inv = 1.0f / float(L.cube);
+  for (int task = tid; task < 64 * CH; task += nthr) {
+    const int r = task / CH, ch = task - r * CH;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = st ? st[r * D + ch * 8 + i] : 0.f;
+    if (xc) {
+      const float* c = xc + (u * L.nc + cube) * D + ch * 8;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] += c[i] * inv;
+    }
+    int64_t row = u * L.seqp + int64_t(cube) * 64 + r;
+    if (raster) {
+      const int64_t rr = raster_of_tile(L, int64_t(cube) * 64 + r);
+      if (rr < 0) continue;
+      row = u * L.seq + rr;
+    }
+    store16(dst + row * D + ch * 8, v);
+  }
+}
+
+// ============================================================================ dK / dV
+template <int D>
+struct KVCfg {
+  static constexpr int kChunks = D / 64;
+  static constexpr int kKV = 64 * D * 2;        // one cube
+  static constexpr int kPair = 128 * D * 2;     // one pair of cubes
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kOffK + kKV;
+  static constexpr int kOffQ = kOffV + kKV;             // 2 stages
+  static constexpr int kOffO = kOffQ + 2 * kPair;       // 2 stages
+  static constexpr int kOffP = kOffO + 2 * kPair;       // 128 x 128 B
+  static constexpr int kOffS = kOffP + 16384;
+  static constexpr int kOffZ = kOffS + 16384;
+  static constexpr int kTiles = kOffZ + (D == 64 ? 16384 : 0);
+  static constexpr int kPairChunk = 16384;  // 128 rows x 128 B
+  static constexpr int kCubeChunk = 8192;   // 64 rows x 128 B
+};
+
+struct KVSmall {
+  uint64_t kv_full, final_bar, pd_full, pd_empty;
+  uint64_t q_full[2], q_empty[2], s_full[2], s_free[2];
+  uint32_t tmem;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    fine_dkdv_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                           DevLayout L, int k_sel, float scale, float scale_log2, const float* __restrict__ lse,
+                           const float* __restrict__ delta, const int32_t* __restrict__ offs,
+                           const int32_t* __restrict__ idx, const float* __restrict__ dkc,
+                           const float* __restrict__ dvc, int raster, __nv_bfloat16* __restrict__ dk,
+                           __nv_bfloat16* __restrict__ dv) {
+  using C = KVCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem + C::kOffK;
+  uint8_t* sV = smem + C::kOffV;
+  uint8_t* sQ = smem + C::kOffQ;
+  uint8_t* sO = smem + C::kOffO;
+  uint8_t* sP = smem + C::kOffP;
+  uint8_t* sS = smem + C::kOffS;
+  uint8_t* sZ = smem + C::kOffZ;
+  KVSmall* sm = reinterpret_cast<KVSmall*>(smem + C::kTiles);
+
+  const int warp = int(warp_id()), lane = int(lane_id());
+  const int kc = blockIdx.x;
+  const int64_t u = blockIdx.y;
+  const int32_t* list = idx + u * int64_t(L.nc) * k_sel;
+  const int beg = offs[u * (L.nc + 1) + kc], end = offs[u * (L.nc + 1) + kc + 1];
+  const int nq = end - beg;
+  const int npairs = (nq + 1) >> 1;
+  const int row0 = int(u * L.seqp);
+
+  if (warp == 6) tmem_alloc<512>(&sm->tmem);
+  if (threadIdx.x == 0) {
+    mbar_init(&sm->kv_full, 1);
+    mbar_init(&sm->final_bar, 1);
+    mbar_init(&sm->pd_full, 128);
+    mbar_init(&sm->pd_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm->q_full[b], 1);
+      mbar_init(&sm->q_empty[b], 1);
+      mbar_init(&sm->s_full[b], 1);
+      mbar_init(&sm->s_free[b], 128);
+    }
+    fence_barrier_init();
+  }
+  // zero the second half of both Q/dO stages (a single-cube last pair must see finite data)
+  if (nq & 1) {
+    for (int i = threadIdx.x; i < 4 * C::kChunks * 512; i += blockDim.x) {
+      const int t = i / (C::kChunks * 512), rem = i - t * C::kChunks * 512;
+      uint8_t* base = (t < 2 ? sQ : sO) + (t & 1) * C::kPair;
+      reinterpret_cast<uint4*>(base + (rem / 512) * C::kPairChunk + 8192)[rem % 512] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  if (D == 64)
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) reinterpret_cast<uint4*>(sZ)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = sm->tmem;
+
+  if (warp == 4) {
+    if (lane == 0 && npairs > 0) {
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_do);
+      mbar_arrive_expect_tx(&sm->kv_full, 2 * C::kKV);
+      for (int c = 0; c < C::kChunks; ++c) {
+        tma_load_2d(sK + c * C::kCubeChunk, &tm_k, &sm->kv_full, c * 64, row0 + kc * 64);
+        tma_load_2d(sV + c * C::kCubeChunk, &tm_v, &sm->kv_full, c * 64, row0 + kc * 64);
+      }
+      for (int p = 0; p < npairs; ++p) {
+        const int st = p & 1;
+        const int qa = list[beg + 2 * p];
+        const bool hb = 2 * p + 1 < nq;
+        const int qb = hb ? list[beg + 2 * p + 1] : 0;
+        mbar_wait(&sm->q_empty[st], ((p >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm->q_full[st], (hb ? 2 : 1) * 2 * C::kKV);
+        uint8_t* q_dst = sQ + st * C::kPair;
+        uint8_t* o_dst = sO + st * C::kPair;
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_2d(q_dst + c * C::kPairChunk, &tm_q, &sm->q_full[st], c * 64, row0 + qa * 64);
+          tma_load_2d(o_dst + c * C::kPairChunk, &tm_do, &sm->q_full[st], c * 64, row0 + qa * 64);
+          if (hb) {
+            tma_load_2d(q_dst + c * C::kPairChunk + 8192, &tm_q, &sm->q_full[st], c * 64, row0 + qb * 64);
+            tma_load_2d(o_dst + c * C::kPairChunk + 8192, &tm_do, &sm->q_full[st], c * 64, row0 + qb * 64);
+          }
+        }
+      }
+    }
+  } else if (warp == 6) {
+    if (lane == 0 && npairs > 0) {
+      const uint32_t idSD = make_idesc_bf16(128, 64, false, false);
+      const uint32_t idG = make_idesc_bf16(128, 64, true, true);
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aO = smem_u32(sO);
+      const uint32_t aP = smem_u32(sP), aS = smem_u32(sS);
+      mbar_wait(&sm->kv_full, 0);
+      auto issue_SdP = [&](int p) {
+        const int st = p & 1;
+        mbar_wait(&sm->q_full[st], (p >> 1) & 1);
+        if (p >= 2) mbar_wait(&sm->s_free[st], ((p >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
+#pragma unroll
+        for (int s = 0; s < D / 16; ++s) {
+          const uint32_t off = (s >> 2) * C::kPairChunk + (s & 3) * 32;
+          const uint32_t offc = (s >> 2) * C::kCubeChunk + (s & 3) * 32;
+          umma_bf16(tbase + st * 64, make_sdesc_sw128(q0 + off, 16, 1024), make_sdesc_sw128(aK + offc, 16, 1024),
+                    idSD, s > 0);
+          umma_bf16(tbase + 128 + st * 64, make_sdesc_sw128(o0 + off, 16, 1024),
+                    make_sdesc_sw128(aV + offc, 16, 1024), idSD, s > 0);
+        }
+        umma_commit(&sm->s_full[st]);
+      };
+      issue_SdP(0);
+      for (int p = 0; p < npairs; ++p) {
+        const int st = p & 1;
+        if (p + 1 < npairs) issue_SdP(p + 1);
+        mbar_wait(&sm->pd_full, p & 1);
+        tc_fence_after();
+        const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
+        const uint32_t lbo_q = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - q0;
+        const uint32_t lbo_o = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - o0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const uint32_t acc = (p > 0 || s > 0) ? 1u : 0u;
+          umma_bf16(tbase + 256, make_sdesc_sw128(o0 + s * 2048, lbo_o, 1024),
+                    make_sdesc_sw128(aP + s * 2048, 8192, 1024), idG, acc);
+          umma_bf16(tbase + 320, make_sdesc_sw128(q0 + s * 2048, lbo_q, 1024),
+                    make_sdesc_sw128(aS + s * 2048, 8192, 1024), idG, acc);
+        }
+        umma_commit(&sm->q_empty[st]);
+        umma_commit(&sm->pd_empty);
+      }
+      umma_commit(&sm->final_bar);
+    }
+  } else if (warp < 4) {
+    const int ql = warp * 32 + lane;  // query lane within the pair
+    const uint32_t lrow = tbase + (uint32_t(warp * 32) << 16);
+    for (int p = 0; p < npairs; ++p) {
+      const int st = p & 1;
+      const bool valid = ql < 64 || (2 * p + 1 < nq);
+      const int qcube = valid ? list[beg + 2 * p + (ql >> 6)] : 0;
+      const int64_t trow = int64_t(row0) + int64_t(valid ? qcube : 0) * 64 + (ql & 63);
+      const float lse2 = valid ? lse[trow] * 1.4426950408889634f : 0.f;
+      const float dl = valid ? delta[trow] : 0.f;
+      mbar_wait(&sm->s_full[st], (p >> 1) & 1);
+      tc_fence_after();
+      float s[64], dpv[64];
+      {
+        float t[32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tmem_ld32(lrow + st * 64 + h * 32, t);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[h * 32 + i] = t[i];
+          tmem_ld32(lrow + 128 + st * 64 + h * 32, t);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dpv[h * 32 + i] = t[i];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm->s_free[st]);
+      uint32_t pp[32], pd[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float p0 = valid ? ex2b(fmaf(s[2 * j], scale_log2, -lse2)) : 0.f;
+        const float p1 = valid ? ex2b(fmaf(s[2 * j + 1], scale_log2, -lse2)) : 0.f;
+        pp[j] = pack_bf16(p0, p1);
+        pd[j] = pack_bf16(p0 * (dpv[2 * j] - dl), p1 * (dpv[2 * j + 1] - dl));
+      }
+      if (p > 0) mbar_wait(&sm->pd_empty, (p - 1) & 1);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        *reinterpret_cast<uint4*>(sP + sw128_offset(ql, c * 16)) =
+            make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]);
+        *reinterpret_cast<uint4*>(sS + sw128_offset(ql, c * 16)) =
+            make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&sm->pd_full);
+    }
+    // ---------------------------------------------------------------- epilogue
+    float* stK = reinterpret_cast<float*>(sQ);                 // [64][D] fp32
+    float* stV = reinterpret_cast<float*>(sQ + 64 * D * 4);    // [64][D] fp32
+    if (npairs > 0) {
+      mbar_wait(&sm->final_bar, 0);
+      tc_fence_after();
+      if (ql < D) {
+        stage_transposed<D>(lrow + 320, stK, ql, scale);
+        stage_transposed<D>(lrow + 256, stV, ql, 1.f);
+      }
+    }
+    named_bar_b(1, 128);
+    write_rows<D>(L, u, kc, npairs > 0 ? stK : nullptr, dkc, raster, dk, threadIdx.x, 128);
+    write_rows<D>(L, u, kc, npairs > 0 ? stV : nullptr, dvc, raster, dv, threadIdx.x, 128);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 6) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+// ============================================================================ dQ
+template <int D>
+struct QCfg {
+  static constexpr int kChunks = D / 64;
+  static constexpr int kCube = 64 * D * 2;
+  static constexpr int kPair = 128 * D * 2;
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffO = kOffQ + kCube;
+  static constexpr int kOffK = kOffO + kCube;           // 2 stages
+  static constexpr int kOffV = kOffK + 2 * kPair;       // 2 stages
+  static constexpr int kOffS = kOffV + 2 * kPair;       // 2 stages of dS^T (128 x 128 B)
+  static constexpr int kOffZ = kOffS + 2 * 16384;
+  static constexpr int kTiles = kOffZ + (D == 64 ? 16384 : 0);
+  static constexpr int kPairChunk = 16384;
+  static constexpr int kCubeChunk = 8192;
+};
+
+struct QSmall {
+  alignas(16) float lse2[64];
+  alignas(16) float dl[64];
+  uint64_t qo_full, final_bar;
+  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_free[2], d_full[2], d_empty[2];
+  uint32_t tmem;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    fine_dq_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                         DevLayout L, int k_sel, float scale, float scale_log2, const float* __restrict__ lse,
+                         const float* __restrict__ delta, const int32_t* __restrict__ sel,
+                         const float* __restrict__ dqc, int raster, __nv_bfloat16* __restrict__ dq) {
+  using C = QCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + C::kOffQ;
+  uint8_t* sO = smem + C::kOffO;
+  uint8_t* sK = smem + C::kOffK;
+  uint8_t* sV = smem + C::kOffV;
+  uint8_t* sS = smem + C::kOffS;
+  uint8_t* sZ = smem + C::kOffZ;
+  QSmall* sm = reinterpret_cast<QSmall*>(smem + C::kTiles);
+
+  const int warp = int(warp_id()), lane = int(lane_id());
+  const int qc = blockIdx.x;
+  const int64_t u = blockIdx.y;
+  const int npairs = (k_sel + 1) >> 1;
+  const int32_t* srow = sel + (u * L.nc + qc) * int64_t(k_sel);
+  const int row0 = int(u * L.seqp);
+
+  if (warp == 6) tmem_alloc<512>(&sm->tmem);
+  if (threadIdx.x == 0) {
+    mbar_init(&sm->qo_full, 1);
+    mbar_init(&sm->final_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm->k_full[b], 1);
+      mbar_init(&sm->k_empty[b], 1);
+      mbar_init(&sm->v_full[b], 1);
+      mbar_init(&sm->v_empty[b], 1);
+      mbar_init(&sm->s_full[b], 1);
+      mbar_init(&sm->s_free[b], 128);
+      mbar_init(&sm->d_full[b], 128);
+      mbar_init(&sm->d_empty[b], 1);
+    }
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 64) {
+    const int64_t r = int64_t(row0) + qc * 64 + threadIdx.x;
+    sm->lse2[threadIdx.x] = lse[r] * 1.4426950408889634f;
+    sm->dl[threadIdx.x] = delta[r];
+  }
+  if (k_sel & 1) {  // single-cube last pair: keys 64..127 of both K/V stages must be finite
+    for (int i = threadIdx.x; i < 4 * C::kChunks * 512; i += blockDim.x) {
+      const int t = i / (C::kChunks * 512), rem = i - t * C::kChunks * 512;
+      uint8_t* base = (t < 2 ? sK : sV) + (t & 1) * C::kPair;
+      reinterpret_cast<uint4*>(base + (rem / 512) * C::kPairChunk + 8192)[rem % 512] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  if (D == 64)
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) reinterpret_cast<uint4*>(sZ)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = sm->tmem;
+
+  if (warp == 4) {  // Q, dO, K producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_do);
+      tma_prefetch_desc(&tm_k);
+      mbar_arrive_expect_tx(&sm->qo_full, 2 * C::kCube);
+      for (int c = 0; c < C::kChunks; ++c) {
+        tma_load_2d(sQ + c * C::kCubeChunk, &tm_q, &sm->qo_full, c * 64, row0 + qc * 64);
+        tma_load_2d(sO + c * C::kCubeChunk, &tm_do, &sm->qo_full, c * 64, row0 + qc * 64);
+      }
+      for (int p = 0; p < npairs; ++p) {
+        const int st = p & 1;
+        const int ka = srow[2 * p];
+        const bool hb = 2 * p + 1 < k_sel;
+        const int kb = hb ? srow[2 * p + 1] : 0;
+        mbar_wait(&sm->k_empty[st], ((p >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm->k_full[st], (hb ? 2 : 1) * C::kCube);
+        uint8_t* dst = sK + st * C::kPair;
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_2d(dst + c * C::kPairChunk, &tm_k, &sm->k_full[st], c * 64, row0 + ka * 64);
+          if (hb) tma_load_2d(dst + c * C::kPairChunk + 8192, &tm_k, &sm->k_full[st], c * 64, row0 + kb * 64);
+        }
+      }
+    }
+  } else if (warp == 5) {  // V producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_v);
+      for (int p = 0; p < npairs; ++p) {
+        const int st = p & 1;
+        const int ka = srow[2 * p];
+        const bool hb = 2 * p + 1 < k_sel;
+        const int kb = hb ? srow[2 * p + 1] : 0;
+        mbar_wait(&sm->v_empty[st], ((p >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm->v_full[st], (hb ? 2 : 1) * C::kCube);
+        uint8_t* dst = sV + st * C::kPair;
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_2d(dst + c * C::kPairChunk, &tm_v, &sm->v_full[st], c * 64, row0 + ka * 64);
+          if (hb) tma_load_2d(dst + c * C::kPairChunk + 8192, &tm_v, &sm->v_full[st], c * 64, row0 + kb * 64);
+        }
+      }
+    }
+  } else if (warp == 6) {  // MMA issuer
+    if (lane == 0) {
+      const uint32_t idSD = make_idesc_bf16(128, 64, false, false);
+      const uint32_t idG = make_idesc_bf16(128, 64, true, true);
+      const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO), aK = smem_u32(sK), aV = smem_u32(sV), aS = smem_u32(sS);
+      mbar_wait(&sm->qo_full, 0);
+      auto issue_SdP = [&](int p) {
+        const int st = p & 1;
+        if (p >= 2) mbar_wait(&sm->s_free[st], ((p >> 1) - 1) & 1);
+        mbar_wait(&sm->k_full[st], (p >> 1) & 1);
+        tc_fence_after();
+        const uint32_t k0 = aK + st * C::kPair, v0 = aV + st * C::kPair;
+#pragma unroll
+        for (int s = 0; s < D / 16; ++s) {
+          const uint32_t off = (s >> 2) * C::kPairChunk + (s & 3) * 32;
+          const uint32_t offc = (s >> 2) * C::kCubeChunk + (s & 3) * 32;
+          umma_bf16(tbase + st * 64, make_sdesc_sw128(k0 + off, 16, 1024), make_sdesc_sw128(aQ + offc, 16, 1024),
+                    idSD, s > 0);
+        }
+        mbar_wait(&sm->v_full[st], (p >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int s = 0; s < D / 16; ++s) {
+          const uint32_t off = (s >> 2) * C::kPairChunk + (s & 3) * 32;
+          const uint32_t offc = (s >> 2) * C::kCubeChunk + (s & 3) * 32;
+          umma_bf16(tbase + 128 + st * 64, make_sdesc_sw128(v0 + off, 16, 1024),
+                    make_sdesc_sw128(aO + offc, 16, 1024), idSD, s > 0);
+        }
+        umma_commit(&sm->v_empty[st]);
+        umma_commit(&sm->s_full[st]);
+      };
+      issue_SdP(0);
+      for (int p = 0; p < npairs; ++p) {
+        const int st = p & 1;
+        if (p + 1 < npairs) issue_SdP(p + 1);
+        mbar_wait(&sm->d_full[st], (p >> 1) & 1);
+        tc_fence_after();
+        const uint32_t k0 = aK + st * C::kPair, s0 = aS + st * 16384;
+        const uint32_t lbo = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - k0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          umma_bf16(tbase + 256, make_sdesc_sw128(k0 + s * 2048, lbo, 1024), make_sdesc_sw128(s0 + s * 2048, 8192, 1024),
+                    idG, (p > 0 || s > 0) ? 1u : 0u);
+        umma_commit(&sm->k_empty[st]);
+        umma_commit(&sm->d_empty[st]);
+      }
+      umma_commit(&sm->final_bar);
+    }
+  } else {  // warps 0-3: dS^T
+    const int kl = warp * 32 + lane;
+    const uint32_t lrow = tbase + (uint32_t(warp * 32) << 16);
+    for (int p = 0; p < npairs; ++p) {
+      const int st = p & 1;
+      const bool valid = kl < 64 || (2 * p + 1 < k_sel);
+      mbar_wait(&sm->s_full[st], (p >> 1) & 1);
+      tc_fence_after();
+      float s[64], dpv[64];
+      {
+        float t[32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tmem_ld32(lrow + st * 64 + h * 32, t);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[h * 32 + i] = t[i];
+          tmem_ld32(lrow + 128 + st * 64 + h * 32, t);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dpv[h * 32 + i] = t[i];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm->s_free[st]);
+      uint32_t pd[32];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float4 l4 = *reinterpret_cast<const float4*>(&sm->lse2[2 * j]);
+        const float4 d4 = *reinterpret_cast<const float4*>(&sm->dl[2 * j]);
+        const float p0 = ex2b(fmaf(s[2 * j], scale_log2, -l4.x));
+        const float p1 = ex2b(fmaf(s[2 * j + 1], scale_log2, -l4.y));
+        const float p2 = ex2b(fmaf(s[2 * j + 2], scale_log2, -l4.z));
+        const float p3 = ex2b(fmaf(s[2 * j + 3], scale_log2, -l4.w));
+        pd[j] = valid ? pack_bf16(p0 * (dpv[2 * j] - d4.x), p1 * (dpv[2 * j + 1] - d4.y)) : 0u;
+        pd[j + 1] = valid ? pack_bf16(p2 * (dpv[2 * j + 2] - d4.z), p3 * (dpv[2 * j + 3] - d4.w)) : 0u;
+      }
+      if (p >= 2) mbar_wait(&sm->d_empty[st], ((p >> 1) - 1) & 1);
+      uint8_t* dS = sS + st * 16384;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(dS + sw128_offset(kl, c * 16)) =
+            make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&sm->d_full[st]);
+    }
+    // ---------------------------------------------------------------- epilogue
+    mbar_wait(&sm->final_bar, 0);
+    tc_fence_after();
+    float* stQ = reinterpret_cast<float*>(sK);  // [64][D] fp32
+    if (kl < D) stage_transposed<D>(lrow + 256, stQ, kl, scale);
+    named_bar_b(1, 128);
+    write_rows<D>(L, u, qc, stQ, dqc, raster, dq, threadIdx.x, 128);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 6) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+}  // namespace vsa_dev
 
 namespace vsa_host {
+using namespace vsa_dev;
 
-bool sm100_fine_bwd_supported(const vsa_layout_t&, int64_t, int32_t) { return false; }
+bool sm100_fine_bwd_supported(const vsa_layout_t& L, int64_t d, int32_t dtype) {
+  return dtype == VSA_BF16 && L.cube == 64 && (d == 64 || d == 128);
+}
+
+template <int D>
+static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const void* k, const void* v,
+                      const void* dof, const float* lse, const float* delta, const int32_t* sel, int64_t top_k,
+                      const int32_t* offs, const int32_t* idx, const float* dqc, const float* dkc, const float* dvc,
+                      int32_t raster, void* dq, void* dk, void* dv, cudaStream_t st) {
+  CUtensorMap tq, tk, tv, tdo;
+  const uint64_t rows = uint64_t(bh * Lh.seq_padded);
+  if (!make_tmap_bf16_sw128(&tq, q, rows, D, 64) || !make_tmap_bf16_sw128(&tk, k, rows, D, 64) ||
+      !make_tmap_bf16_sw128(&tv, v, rows, D, 64) || !make_tmap_bf16_sw128(&tdo, dof, rows, D, 64)) {
+    set_error("fine_backward: cuTensorMapEncodeTiled failed");
+    return VSA_EINVAL;
+  }
+  const float scale = 1.0f / std::sqrt(float(D));
+  const float scale_log2 = scale * 1.4426950408889634f;
+  const DevLayout L = to_dev(Lh);
+  dim3 grid(unsigned(Lh.nc), unsigned(bh));
+  {
+    const size_t smem = QCfg<D>::kTiles + sizeof(QSmall) + 1024;
+    auto kern = fine_dq_sm100_kernel<D>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kern<<<grid, kBwdThreads, smem, st>>>(tq, tk, tv, tdo, L, int(top_k), scale, scale_log2, lse, delta, sel, dqc,
+                                         raster, static_cast<__nv_bfloat16*>(dq));
+    int rc = kernel_status("fine_dq_sm100_kernel");
+    if (rc) return rc;
+  }
+  {
+    const size_t smem = KVCfg<D>::kTiles + sizeof(KVSmall) + 1024;
+    auto kern = fine_dkdv_sm100_kernel<D>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kern<<<grid, kBwdThreads, smem, st>>>(tq, tk, tv, tdo, L, int(top_k), scale, scale_log2, lse, delta, offs, idx,
+                                         dkc, dvc, raster, static_cast<__nv_bfloat16*>(dk),
+                                         static_cast<__nv_bfloat16*>(dv));
+  }
+  VSA_LAUNCH_CHECK("fine_dkdv_sm100_kernel");
+}
 
 int launch_fine_backward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, const void* q, const void* k,
                                const void* v, const void* dof, const float* lse, const float* delta,
                                const int32_t* sel, int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx,
                                const float* dqc, const float* dkc, const float* dvc, int32_t raster, void* dq,
                                void* dk, void* dv, cudaStream_t st) {
-  return launch_fine_backward_simt(L, bh, d, VSA_BF16, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx,
-                                   dqc, dkc, dvc, raster, dq, dk, dv, st);
+  if (d == 128)
+    return bwd_launch<128>(L, bh, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc, dvc, raster,
+                           dq, dk, dv, st);
+  return bwd_launch<64>(L, bh, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc, dvc, raster, dq,
+                        dk, dv, st);
 }
 
 }  // namespace vsa_host

@@ -22,6 +22,10 @@ int launch_selection_transpose(const vsa_layout_t& L, int64_t bh, const int32_t*
 int launch_validate_selection(const int32_t* sel, int64_t rows, int64_t top_k, int64_t nc, int32_t* err,
                               cudaStream_t st);
 size_t coarse_bitmap_bytes(const vsa_layout_t& L, int64_t bh);
+// batched fp32 GEMM, one ascending-k fma chain per element (gemm_simt.cu); alpha may be null
+int launch_gemm_f32(int batch, int M, int N, int K, const float* A, int64_t sAb, int64_t sAm, int64_t sAk,
+                    const float* B, int64_t sBb, int64_t sBk, int64_t sBn, float* C, int64_t sCb, int64_t sCm,
+                    const float* alpha, cudaStream_t st);
 
 int launch_backward_prologue(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, int32_t raster,
                              const void* dout, const void* gc, const void* gf, const float* oc_cube,
