@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                            __nv_bfloat16* __restrict__ dv) {
   using C = KVCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sK = smem + C::kOffK;
   uint8_t* sV = smem + C::kOffV;
   uint8_t* sQ = smem + C::kOffQ;
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                          const float* __restrict__ dqc, int raster, __nv_bfloat16* __restrict__ dq) {
   using C = QCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sQ = smem + C::kOffQ;
   uint8_t* sO = smem + C::kOffO;
   uint8_t* sK = smem + C::kOffK;

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
                           __nv_bfloat16* __restrict__ out) {
   using C = FwdCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sQ = smem + C::kOffQ;
   uint8_t* sK = smem + C::kOffK;
   uint8_t* sV = smem + C::kOffV;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 #pragma unroll
         for (int i = 0; i < 32; ++i) x[32 + i] = t[i];
       }
-      bool need = false;
+      float mx = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 64; i += 4) {
         const float4 mq = *reinterpret_cast<const float4*>(&sm->m[i]);
@@ -256,22 +256,25 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         x[i + 1] = fmaf(x[i + 1], scale_log2, -mq.y);
         x[i + 2] = fmaf(x[i + 2], scale_log2, -mq.z);
         x[i + 3] = fmaf(x[i + 3], scale_log2, -mq.w);
-        need |= (x[i] > tau) | (x[i + 1] > tau) | (x[i + 2] > tau) | (x[i + 3] > tau);
+        mx = fmaxf(mx, fmaxf(fmaxf(x[i], x[i + 1]), fmaxf(x[i + 2], x[i + 3])));
       }
-      need = need && valid;
+      const bool need = valid && mx > tau;  // `valid` is warp-uniform
       if (__ballot_sync(0xffffffffu, need) != 0u && lane == 0) vflag[p & 1] = p + 1;
       named_bar(1, 128);
       const bool upd = vflag[p & 1] == p + 1;
       if (upd) {
         // exact per-query max of this pair over all 128 key lanes
-        {
+        if (valid) {
           float t[32];
           tmem_ld32(lrow + b * 64, t);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[i] = valid ? t[i] * scale_log2 : -INFINITY;
+          for (int i = 0; i < 32; ++i) x[i] = t[i] * scale_log2;
           tmem_ld32(lrow + b * 64 + 32, t);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[32 + i] = valid ? t[i] * scale_log2 : -INFINITY;
+          for (int i = 0; i < 32; ++i) x[32 + i] = t[i] * scale_log2;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) x[i] = -INFINITY;
         }
         reduce_scatter64<true>(x, lane);
         const int q0 = rs_q0(lane);
@@ -304,14 +307,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
             tmem_st32(lrow + 192 + h * 32, t);
           }
         }
-        {
+        if (valid) {
           float t[32];
           tmem_ld32(lrow + b * 64, t);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[i] = valid ? fmaf(t[i], scale_log2, -sm->m[i]) : -INFINITY;
+          for (int i = 0; i < 32; ++i) x[i] = fmaf(t[i], scale_log2, -sm->m[i]);
           tmem_ld32(lrow + b * 64 + 32, t);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[32 + i] = valid ? fmaf(t[i], scale_log2, -sm->m[32 + i]) : -INFINITY;
+          for (int i = 0; i < 32; ++i) x[32 + i] = fmaf(t[i], scale_log2, -sm->m[32 + i]);
         }
       } else if (p > 0) {
         mbar_wait(&sm->p_empty, (p - 1) & 1);
@@ -320,29 +323,42 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       tc_fence_before();
       mbar_arrive(&sm->s_free[b]);
       // probabilities, row-sum partials (TMEM), P^T tile (bf16, MN-major SW128)
+      if (valid) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float lv[32];
-        if (p > 0) {
-          tmem_ld32(lrow + 192 + h * 32, lv);
-        } else {
+        for (int h = 0; h < 2; ++h) {
+          float lv[32];
+          if (p > 0) {
+            tmem_ld32(lrow + 192 + h * 32, lv);
+          } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) lv[i] = 0.f;
+            for (int i = 0; i < 32; ++i) lv[i] = 0.f;
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = ex2(x[h * 32 + 2 * i]);
+            const float p1 = ex2(x[h * 32 + 2 * i + 1]);
+            lv[2 * i] += p0;
+            lv[2 * i + 1] += p1;
+            pk[i] = pack_bf16(p0, p1);
+          }
+          tmem_st32(lrow + 192 + h * 32, lv);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(sP + sw128_offset(kl, (h * 4 + j) * 16)) =
+                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         }
-        uint32_t pk[16];
+      } else {  // the missing half of a single-cube last pair: P = 0, sums untouched
+        if (p == 0) {
+          float z[32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float p0 = valid ? ex2(x[h * 32 + 2 * i]) : 0.f;
-          const float p1 = valid ? ex2(x[h * 32 + 2 * i + 1]) : 0.f;
-          lv[2 * i] += p0;
-          lv[2 * i + 1] += p1;
-          pk[i] = pack_bf16(p0, p1);
+          for (int i = 0; i < 32; ++i) z[i] = 0.f;
+          tmem_st32(lrow + 192, z);
+          tmem_st32(lrow + 224, z);
         }
-        tmem_st32(lrow + 192 + h * 32, lv);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          *reinterpret_cast<uint4*>(sP + sw128_offset(kl, (h * 4 + j) * 16)) =
-              make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint4*>(sP + sw128_offset(kl, j * 16)) = make_uint4(0, 0, 0, 0);
       }
       fence_proxy_async_smem();
       tc_fence_before();
@@ -370,7 +386,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     const float kLn2 = 0.6931471805599453f;
     if (kl < 64) {
       const float l = (sm->red[0][kl] + sm->red[1][kl]) + (sm->red[2][kl] + sm->red[3][kl]);
-      sm->alpha[kl] = l;
+      sm->alpha[kl] = 1.0f / l;
       const int64_t trow = int64_t(row0) + qc * 64 + kl;
       lse[trow] = sm->m[kl] * kLn2 + logf(l);
       if (rmax) rmax[trow] = sm->m[kl] * kLn2;
@@ -384,7 +400,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       for (int h = 0; h < 2; ++h) {
         tmem_ld32(lrow + 128 + h * 32, t);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) stO[(h * 32 + i) * D + kl] = t[i] / sm->alpha[h * 32 + i];
+        for (int i = 0; i < 32; ++i) stO[(h * 32 + i) * D + kl] = t[i] * sm->alpha[h * 32 + i];
       }
     }
     named_bar(1, 128);
