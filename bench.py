@@ -85,17 +85,20 @@ class ClockSampler:
         self._stop = threading.Event()
         self._nvml = None
 
+    def _sample(self):
+        nv, h = self._nvml, self._h
+        self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+        r = int(self._get_r(h))
+        for bit, name in self.REASONS.items():
+            if r & bit:
+                self.reasons.add(name)
+
     def _poll(self):
-        nv = self._nvml
-        h = nv.nvmlDeviceGetHandleByIndex(self.idx)
-        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
-        self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
         while not self._stop.is_set():
-            self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
-            r = int(get_r(h))
-            for bit, name in self.REASONS.items():
-                if r & bit:
-                    self.reasons.add(name)
+            try:
+                self._sample()
+            except Exception:
+                return
             time.sleep(0.002)
 
     def __enter__(self):
@@ -104,6 +107,10 @@ class ClockSampler:
 
             pynvml.nvmlInit()
             self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self._get_r = (getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None)
+                           or pynvml.nvmlDeviceGetCurrentClocksThrottleReasons)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
             self._t = threading.Thread(target=self._poll, daemon=True)
             self._t.start()
         except Exception:
@@ -122,6 +129,10 @@ class ClockSampler:
         self._stop.set()
         if self._nvml is not None:
             self._t.join(timeout=2)
+            try:
+                self._sample()  # at least one sample at the end of the timed region
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:

@@ -20,11 +20,12 @@
 // are written by the compute threads directly in the MN-major SW128 B layout.
 // Key cubes selected by no query get exactly zero fine gradient (test_fine.cpp:149-169).
 //
-// Roles (224 threads, 1 CTA/SM): warps 0-3 compute + epilogue (TMEM quadrant =
-// warp), warp 4 TMA producer A, warp 5 TMA producer B, warp 6 TMEM alloc + MMA
-// issuer. Operand stages are double-buffered; S / dP are double-buffered in TMEM
-// and the MMA issuer runs one pair ahead so the exp2 / dS math of pair p overlaps
-// the S, dP products of pair p+1.
+// Roles (352 threads, 1 CTA/SM): warps 0-7 = two compute warpgroups in ping-pong
+// (warpgroup g owns the pairs p = g mod 2, TMEM quadrant = warp % 4), warp 8 / 9
+// TMA producers, warp 10 TMEM allocator + single-thread MMA issuer. S / dP are
+// double-buffered in TMEM by pair parity, operand stages and P / dS smem buffers
+// likewise, and the MMA issuer runs one pair ahead: the exp2 / dS math of pairs
+// p and p+1 overlaps the products of p-1, p+1 and p+2.
 #include <cmath>
 
 #include "common.cuh"
@@ -34,7 +35,8 @@
 
 namespace vsa_dev {
 
-constexpr int kBwdThreads = 224;
+constexpr int kBwdThreads = 352;
+constexpr int kCompute = 256;  // two warpgroups
 
 __device__ __forceinline__ float ex2b(float x) {
   float y;
@@ -43,16 +45,26 @@ __device__ __forceinline__ float ex2b(float x) {
 }
 __device__ __forceinline__ void named_bar_b(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
-// [64 rows][D] fp32 staging of a TMEM [D lanes x 64 cols] accumulator (thread = lane = d row).
+__device__ __forceinline__ void tmem_ld32_raw(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// TMEM [D lanes x 32 cols] accumulator slice -> [64 rows][D] fp32 staging (rows c0..c0+31).
 template <int D>
-__device__ __forceinline__ void stage_transposed(uint32_t taddr_lane, float* st, int dl, float scale) {
+__device__ __forceinline__ void stage_cols(uint32_t taddr_lane, int c0, float* st, int dl, float scale) {
   float t[32];
+  tmem_ld32(taddr_lane + c0, t);
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    tmem_ld32(taddr_lane + h * 32, t);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) st[(h * 32 + i) * D + dl] = t[i] * scale;
-  }
+  for (int i = 0; i < 32; ++i) st[(c0 + i) * D + dl] = t[i] * scale;
 }
 
 // Write a [64][D] fp32 staged tile as bf16 rows of cube `cube`, adding xc/64 (mean unpool).
@@ -86,23 +98,23 @@ __device__ __forceinline__ void write_rows(const DevLayout& L, int64_t u, int cu
 template <int D>
 struct KVCfg {
   static constexpr int kChunks = D / 64;
-  static constexpr int kKV = 64 * D * 2;        // one cube
+  static constexpr int kCube = 64 * D * 2;      // one cube
   static constexpr int kPair = 128 * D * 2;     // one pair of cubes
   static constexpr int kOffK = 0;
-  static constexpr int kOffV = kOffK + kKV;
-  static constexpr int kOffQ = kOffV + kKV;             // 2 stages
+  static constexpr int kOffV = kOffK + kCube;
+  static constexpr int kOffQ = kOffV + kCube;           // 2 stages
   static constexpr int kOffO = kOffQ + 2 * kPair;       // 2 stages
-  static constexpr int kOffP = kOffO + 2 * kPair;       // 128 x 128 B
-  static constexpr int kOffS = kOffP + 16384;
-  static constexpr int kOffZ = kOffS + 16384;
+  static constexpr int kOffP = kOffO + 2 * kPair;       // 2 x (128 x 128 B)
+  static constexpr int kOffS = kOffP + 2 * 16384;       // 2 x (128 x 128 B)
+  static constexpr int kOffZ = kOffS + 2 * 16384;
   static constexpr int kTiles = kOffZ + (D == 64 ? 16384 : 0);
   static constexpr int kPairChunk = 16384;  // 128 rows x 128 B
   static constexpr int kCubeChunk = 8192;   // 64 rows x 128 B
 };
 
 struct KVSmall {
-  uint64_t kv_full, final_bar, pd_full, pd_empty;
-  uint64_t q_full[2], q_empty[2], s_full[2], s_free[2];
+  uint64_t kv_full, final_bar;
+  uint64_t q_full[2], q_empty[2], s_full[2], s_free[2], pd_full[2], pd_empty[2];
   uint32_t tmem;
 };
 
@@ -136,17 +148,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int npairs = (nq + 1) >> 1;
   const int row0 = int(u * L.seqp);
 
-  if (warp == 6) tmem_alloc<512>(&sm->tmem);
+  if (warp == 10) tmem_alloc<512>(&sm->tmem);
   if (threadIdx.x == 0) {
     mbar_init(&sm->kv_full, 1);
     mbar_init(&sm->final_bar, 1);
-    mbar_init(&sm->pd_full, 128);
-    mbar_init(&sm->pd_empty, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm->q_full[b], 1);
       mbar_init(&sm->q_empty[b], 1);
       mbar_init(&sm->s_full[b], 1);
       mbar_init(&sm->s_free[b], 128);
+      mbar_init(&sm->pd_full[b], 128);
+      mbar_init(&sm->pd_empty[b], 1);
     }
     fence_barrier_init();
   }
@@ -166,13 +178,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   tc_fence_after();
   const uint32_t tbase = sm->tmem;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0 && npairs > 0) {
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_do);
-      mbar_arrive_expect_tx(&sm->kv_full, 2 * C::kKV);
+      mbar_arrive_expect_tx(&sm->kv_full, 2 * C::kCube);
       for (int c = 0; c < C::kChunks; ++c) {
         tma_load_2d(sK + c * C::kCubeChunk, &tm_k, &sm->kv_full, c * 64, row0 + kc * 64);
         tma_load_2d(sV + c * C::kCubeChunk, &tm_v, &sm->kv_full, c * 64, row0 + kc * 64);
@@ -183,7 +195,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const bool hb = 2 * p + 1 < nq;
         const int qb = hb ? list[beg + 2 * p + 1] : 0;
         mbar_wait(&sm->q_empty[st], ((p >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&sm->q_full[st], (hb ? 2 : 1) * 2 * C::kKV);
+        mbar_arrive_expect_tx(&sm->q_full[st], (hb ? 2 : 1) * 2 * C::kCube);
         uint8_t* q_dst = sQ + st * C::kPair;
         uint8_t* o_dst = sO + st * C::kPair;
         for (int c = 0; c < C::kChunks; ++c) {
@@ -196,98 +208,104 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
     }
-  } else if (warp == 6) {
+  } else if (warp == 10) {
     if (lane == 0 && npairs > 0) {
       const uint32_t idSD = make_idesc_bf16(128, 64, false, false);
       const uint32_t idG = make_idesc_bf16(128, 64, true, true);
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aO = smem_u32(sO);
       const uint32_t aP = smem_u32(sP), aS = smem_u32(sS);
       mbar_wait(&sm->kv_full, 0);
-      auto issue_SdP = [&](int p) {
-        const int st = p & 1;
-        mbar_wait(&sm->q_full[st], (p >> 1) & 1);
-        if (p >= 2) mbar_wait(&sm->s_free[st], ((p >> 1) - 1) & 1);
-        tc_fence_after();
-        const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
+      // Event-driven issue of two in-order streams: {S, dP}(ns) and {dV, dK}(no).
+      int ns = 0, no = 0;
+      while (no < npairs) {
+        if (ns < npairs && mbar_try_wait(&sm->q_full[ns & 1], (ns >> 1) & 1) &&
+            (ns < 2 || mbar_try_wait(&sm->s_free[ns & 1], ((ns >> 1) - 1) & 1))) {
+          const int st = ns & 1;
+          tc_fence_after();
+          const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
 #pragma unroll
-        for (int s = 0; s < D / 16; ++s) {
-          const uint32_t off = (s >> 2) * C::kPairChunk + (s & 3) * 32;
-          const uint32_t offc = (s >> 2) * C::kCubeChunk + (s & 3) * 32;
-          umma_bf16(tbase + st * 64, make_sdesc_sw128(q0 + off, 16, 1024), make_sdesc_sw128(aK + offc, 16, 1024),
-                    idSD, s > 0);
-          umma_bf16(tbase + 128 + st * 64, make_sdesc_sw128(o0 + off, 16, 1024),
-                    make_sdesc_sw128(aV + offc, 16, 1024), idSD, s > 0);
+          for (int s = 0; s < D / 16; ++s) {
+            const uint32_t off = (s >> 2) * C::kPairChunk + (s & 3) * 32;
+            const uint32_t offc = (s >> 2) * C::kCubeChunk + (s & 3) * 32;
+            umma_bf16(tbase + st * 64, make_sdesc_sw128(q0 + off, 16, 1024), make_sdesc_sw128(aK + offc, 16, 1024),
+                      idSD, s > 0);
+            umma_bf16(tbase + 128 + st * 64, make_sdesc_sw128(o0 + off, 16, 1024),
+                      make_sdesc_sw128(aV + offc, 16, 1024), idSD, s > 0);
+          }
+          umma_commit(&sm->s_full[st]);
+          ++ns;
         }
-        umma_commit(&sm->s_full[st]);
-      };
-      issue_SdP(0);
-      for (int p = 0; p < npairs; ++p) {
-        const int st = p & 1;
-        if (p + 1 < npairs) issue_SdP(p + 1);
-        mbar_wait(&sm->pd_full, p & 1);
-        tc_fence_after();
-        const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
-        const uint32_t lbo_q = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - q0;
-        const uint32_t lbo_o = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - o0;
+        if (no < ns && mbar_try_wait(&sm->pd_full[no & 1], (no >> 1) & 1)) {
+          const int st = no & 1;
+          tc_fence_after();
+          const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
+          const uint32_t p0 = aP + st * 16384, s0 = aS + st * 16384;
+          const uint32_t lbo_q = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - q0;
+          const uint32_t lbo_o = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - o0;
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const uint32_t acc = (p > 0 || s > 0) ? 1u : 0u;
-          umma_bf16(tbase + 256, make_sdesc_sw128(o0 + s * 2048, lbo_o, 1024),
-                    make_sdesc_sw128(aP + s * 2048, 8192, 1024), idG, acc);
-          umma_bf16(tbase + 320, make_sdesc_sw128(q0 + s * 2048, lbo_q, 1024),
-                    make_sdesc_sw128(aS + s * 2048, 8192, 1024), idG, acc);
+          for (int s = 0; s < 8; ++s) {
+            const uint32_t acc = (no > 0 || s > 0) ? 1u : 0u;
+            umma_bf16(tbase + 256, make_sdesc_sw128(o0 + s * 2048, lbo_o, 1024),
+                      make_sdesc_sw128(p0 + s * 2048, 8192, 1024), idG, acc);
+            umma_bf16(tbase + 320, make_sdesc_sw128(q0 + s * 2048, lbo_q, 1024),
+                      make_sdesc_sw128(s0 + s * 2048, 8192, 1024), idG, acc);
+          }
+          umma_commit(&sm->q_empty[st]);
+          umma_commit(&sm->pd_empty[st]);
+          ++no;
         }
-        umma_commit(&sm->q_empty[st]);
-        umma_commit(&sm->pd_empty);
       }
       umma_commit(&sm->final_bar);
     }
-  } else if (warp < 4) {
-    const int ql = warp * 32 + lane;  // query lane within the pair
-    const uint32_t lrow = tbase + (uint32_t(warp * 32) << 16);
-    for (int p = 0; p < npairs; ++p) {
-      const int st = p & 1;
-      const bool valid = ql < 64 || (2 * p + 1 < nq);
-      const int qcube = valid ? list[beg + 2 * p + (ql >> 6)] : 0;
-      const int64_t trow = int64_t(row0) + int64_t(valid ? qcube : 0) * 64 + (ql & 63);
-      const float lse2 = valid ? lse[trow] * 1.4426950408889634f : 0.f;
-      const float dl = valid ? delta[trow] : 0.f;
-      mbar_wait(&sm->s_full[st], (p >> 1) & 1);
+  } else if (warp < 8) {
+    const int g = warp >> 2;                 // warpgroup: pairs p = g (mod 2)
+    const int ql = (warp & 3) * 32 + lane;   // query lane within the pair
+    const uint32_t lrow = tbase + (uint32_t((warp & 3) * 32) << 16);
+    uint8_t* myP = sP + g * 16384;
+    uint8_t* myS = sS + g * 16384;
+    for (int p = g; p < npairs; p += 2) {
+      const bool valid = ql < 64 || (2 * p + 1 < nq);  // warp-uniform
+      float lse2 = 0.f, dl = 0.f;
+      if (valid) {
+        const int qcube = list[beg + 2 * p + (ql >> 6)];
+        const int64_t trow = int64_t(row0) + int64_t(qcube) * 64 + (ql & 63);
+        lse2 = lse[trow] * 1.4426950408889634f;
+        dl = delta[trow];
+      }
+      mbar_wait(&sm->s_full[g], (p >> 1) & 1);
       tc_fence_after();
-      float s[64], dpv[64];
-      {
-        float t[32];
+      uint32_t pp[32], pd[32];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          tmem_ld32(lrow + st * 64 + h * 32, t);
+      for (int h = 0; h < 2; ++h) {
+        uint32_t rs[32], rd[32];
+        tmem_ld32_raw(lrow + g * 64 + h * 32, rs);
+        tmem_ld32_raw(lrow + 128 + g * 64 + h * 32, rd);
+        tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) s[h * 32 + i] = t[i];
-          tmem_ld32(lrow + 128 + st * 64 + h * 32, t);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) dpv[h * 32 + i] = t[i];
+        for (int j = 0; j < 16; ++j) {
+          const float p0 = ex2b(fmaf(__uint_as_float(rs[2 * j]), scale_log2, -lse2));
+          const float p1 = ex2b(fmaf(__uint_as_float(rs[2 * j + 1]), scale_log2, -lse2));
+          pp[h * 16 + j] = pack_bf16(p0, p1);
+          pd[h * 16 + j] = pack_bf16(p0 * (__uint_as_float(rd[2 * j]) - dl), p1 * (__uint_as_float(rd[2 * j + 1]) - dl));
         }
       }
       tc_fence_before();
-      mbar_arrive(&sm->s_free[st]);
-      uint32_t pp[32], pd[32];
+      mbar_arrive(&sm->s_free[g]);
+      if (!valid) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float p0 = valid ? ex2b(fmaf(s[2 * j], scale_log2, -lse2)) : 0.f;
-        const float p1 = valid ? ex2b(fmaf(s[2 * j + 1], scale_log2, -lse2)) : 0.f;
-        pp[j] = pack_bf16(p0, p1);
-        pd[j] = pack_bf16(p0 * (dpv[2 * j] - dl), p1 * (dpv[2 * j + 1] - dl));
+        for (int j = 0; j < 32; ++j) pp[j] = pd[j] = 0u;
       }
-      if (p > 0) mbar_wait(&sm->pd_empty, (p - 1) & 1);
+      if (p >= 2) mbar_wait(&sm->pd_empty[g], ((p >> 1) - 1) & 1);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        *reinterpret_cast<uint4*>(sP + sw128_offset(ql, c * 16)) =
+        *reinterpret_cast<uint4*>(myP + sw128_offset(ql, c * 16)) =
             make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]);
-        *reinterpret_cast<uint4*>(sS + sw128_offset(ql, c * 16)) =
+        *reinterpret_cast<uint4*>(myS + sw128_offset(ql, c * 16)) =
             make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
       }
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(&sm->pd_full);
+      mbar_arrive(&sm->pd_full[g]);
     }
     // ---------------------------------------------------------------- epilogue
     float* stK = reinterpret_cast<float*>(sQ);                 // [64][D] fp32
@@ -295,18 +313,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (npairs > 0) {
       mbar_wait(&sm->final_bar, 0);
       tc_fence_after();
-      if (ql < D) {
-        stage_transposed<D>(lrow + 320, stK, ql, scale);
-        stage_transposed<D>(lrow + 256, stV, ql, 1.f);
+      if (ql < D) {  // warpgroup 0 stages dK^T, warpgroup 1 dV^T
+        stage_cols<D>(lrow + (g ? 256 : 320), 0, g ? stV : stK, ql, g ? 1.f : scale);
+        stage_cols<D>(lrow + (g ? 256 : 320), 32, g ? stV : stK, ql, g ? 1.f : scale);
       }
     }
-    named_bar_b(1, 128);
-    write_rows<D>(L, u, kc, npairs > 0 ? stK : nullptr, dkc, raster, dk, threadIdx.x, 128);
-    write_rows<D>(L, u, kc, npairs > 0 ? stV : nullptr, dvc, raster, dv, threadIdx.x, 128);
+    named_bar_b(1, kCompute);
+    write_rows<D>(L, u, kc, npairs > 0 ? stK : nullptr, dkc, raster, dk, threadIdx.x, kCompute);
+    write_rows<D>(L, u, kc, npairs > 0 ? stV : nullptr, dvc, raster, dv, threadIdx.x, kCompute);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 6) {
+  if (warp == 10) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }
@@ -320,8 +338,9 @@ struct QCfg {
   static constexpr int kPair = 128 * D * 2;
   static constexpr int kOffQ = 0;
   static constexpr int kOffO = kOffQ + kCube;
-  static constexpr int kOffK = kOffO + kCube;           // 2 stages
-  static constexpr int kOffV = kOffK + 2 * kPair;       // 2 stages
+  static constexpr int kKStages = 3;                    // K is held until dQ(p): deeper ring
+  static constexpr int kOffK = kOffO + kCube;           // 3 stages
+  static constexpr int kOffV = kOffK + kKStages * kPair;  // 2 stages
   static constexpr int kOffS = kOffV + 2 * kPair;       // 2 stages of dS^T (128 x 128 B)
   static constexpr int kOffZ = kOffS + 2 * 16384;
   static constexpr int kTiles = kOffZ + (D == 64 ? 16384 : 0);
@@ -333,7 +352,7 @@ struct QSmall {
   alignas(16) float lse2[64];
   alignas(16) float dl[64];
   uint64_t qo_full, final_bar;
-  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_free[2], d_full[2], d_empty[2];
+  uint64_t k_full[3], k_empty[3], v_full[2], v_empty[2], s_full[2], s_free[2], d_full[2], d_empty[2];
   uint32_t tmem;
 };
 
@@ -362,19 +381,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int32_t* srow = sel + (u * L.nc + qc) * int64_t(k_sel);
   const int row0 = int(u * L.seqp);
 
-  if (warp == 6) tmem_alloc<512>(&sm->tmem);
+  if (warp == 10) tmem_alloc<512>(&sm->tmem);
   if (threadIdx.x == 0) {
     mbar_init(&sm->qo_full, 1);
     mbar_init(&sm->final_bar, 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm->k_full[b], 1);
-      mbar_init(&sm->k_empty[b], 1);
       mbar_init(&sm->v_full[b], 1);
       mbar_init(&sm->v_empty[b], 1);
       mbar_init(&sm->s_full[b], 1);
       mbar_init(&sm->s_free[b], 128);
       mbar_init(&sm->d_full[b], 128);
       mbar_init(&sm->d_empty[b], 1);
+    }
+    for (int b = 0; b < C::kKStages; ++b) {
+      mbar_init(&sm->k_full[b], 1);
+      mbar_init(&sm->k_empty[b], 1);
     }
     fence_barrier_init();
   }
@@ -383,10 +404,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     sm->lse2[threadIdx.x] = lse[r] * 1.4426950408889634f;
     sm->dl[threadIdx.x] = delta[r];
   }
-  if (k_sel & 1) {  // single-cube last pair: keys 64..127 of both K/V stages must be finite
-    for (int i = threadIdx.x; i < 4 * C::kChunks * 512; i += blockDim.x) {
+  if (k_sel & 1) {  // single-cube last pair: keys 64..127 of every K/V stage must be finite
+    for (int i = threadIdx.x; i < (C::kKStages + 2) * C::kChunks * 512; i += blockDim.x) {
       const int t = i / (C::kChunks * 512), rem = i - t * C::kChunks * 512;
-      uint8_t* base = (t < 2 ? sK : sV) + (t & 1) * C::kPair;
+      uint8_t* base = t < C::kKStages ? sK + t * C::kPair : sV + (t - C::kKStages) * C::kPair;
       reinterpret_cast<uint4*>(base + (rem / 512) * C::kPairChunk + 8192)[rem % 512] = make_uint4(0, 0, 0, 0);
     }
   }
@@ -398,7 +419,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   tc_fence_after();
   const uint32_t tbase = sm->tmem;
 
-  if (warp == 4) {  // Q, dO, K producer
+  if (warp == 8) {  // Q, dO, K producer
     if (lane == 0) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_do);
@@ -409,11 +430,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_load_2d(sO + c * C::kCubeChunk, &tm_do, &sm->qo_full, c * 64, row0 + qc * 64);
       }
       for (int p = 0; p < npairs; ++p) {
-        const int st = p & 1;
+        const int st = p % C::kKStages;
         const int ka = srow[2 * p];
         const bool hb = 2 * p + 1 < k_sel;
         const int kb = hb ? srow[2 * p + 1] : 0;
-        mbar_wait(&sm->k_empty[st], ((p >> 1) & 1) ^ 1);
+        mbar_wait(&sm->k_empty[st], ((p / C::kKStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&sm->k_full[st], (hb ? 2 : 1) * C::kCube);
         uint8_t* dst = sK + st * C::kPair;
         for (int c = 0; c < C::kChunks; ++c) {
@@ -422,7 +443,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
     }
-  } else if (warp == 5) {  // V producer
+  } else if (warp == 9) {  // V producer
     if (lane == 0) {
       tma_prefetch_desc(&tm_v);
       for (int p = 0; p < npairs; ++p) {
@@ -439,110 +460,106 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
     }
-  } else if (warp == 6) {  // MMA issuer
+  } else if (warp == 10) {  // MMA issuer
     if (lane == 0) {
       const uint32_t idSD = make_idesc_bf16(128, 64, false, false);
       const uint32_t idG = make_idesc_bf16(128, 64, true, true);
       const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO), aK = smem_u32(sK), aV = smem_u32(sV), aS = smem_u32(sS);
       mbar_wait(&sm->qo_full, 0);
-      auto issue_SdP = [&](int p) {
-        const int st = p & 1;
-        if (p >= 2) mbar_wait(&sm->s_free[st], ((p >> 1) - 1) & 1);
-        mbar_wait(&sm->k_full[st], (p >> 1) & 1);
-        tc_fence_after();
-        const uint32_t k0 = aK + st * C::kPair, v0 = aV + st * C::kPair;
+      // Event-driven issue of two in-order streams: {S, dP}(ns) and dQ(no); neither blocks the other.
+      int ns = 0, no = 0;
+      while (no < npairs) {
+        if (ns < npairs) {
+          const int st = ns & 1, ks = ns % C::kKStages;
+          if ((ns < 2 || mbar_try_wait(&sm->s_free[st], ((ns >> 1) - 1) & 1)) &&
+              mbar_try_wait(&sm->k_full[ks], (ns / C::kKStages) & 1) && mbar_try_wait(&sm->v_full[st], (ns >> 1) & 1)) {
+            tc_fence_after();
+            const uint32_t k0 = aK + ks * C::kPair, v0 = aV + st * C::kPair;
 #pragma unroll
-        for (int s = 0; s < D / 16; ++s) {
-          const uint32_t off = (s >> 2) * C::kPairChunk + (s & 3) * 32;
-          const uint32_t offc = (s >> 2) * C::kCubeChunk + (s & 3) * 32;
-          umma_bf16(tbase + st * 64, make_sdesc_sw128(k0 + off, 16, 1024), make_sdesc_sw128(aQ + offc, 16, 1024),
-                    idSD, s > 0);
+            for (int s = 0; s < D / 16; ++s) {
+              const uint32_t off = (s >> 2) * C::kPairChunk + (s & 3) * 32;
+              const uint32_t offc = (s >> 2) * C::kCubeChunk + (s & 3) * 32;
+              umma_bf16(tbase + st * 64, make_sdesc_sw128(k0 + off, 16, 1024),
+                        make_sdesc_sw128(aQ + offc, 16, 1024), idSD, s > 0);
+              umma_bf16(tbase + 128 + st * 64, make_sdesc_sw128(v0 + off, 16, 1024),
+                        make_sdesc_sw128(aO + offc, 16, 1024), idSD, s > 0);
+            }
+            umma_commit(&sm->v_empty[st]);
+            umma_commit(&sm->s_full[st]);
+            ++ns;
+          }
         }
-        mbar_wait(&sm->v_full[st], (p >> 1) & 1);
-        tc_fence_after();
+        if (no < ns && mbar_try_wait(&sm->d_full[no & 1], (no >> 1) & 1)) {
+          tc_fence_after();
+          const int ks = no % C::kKStages;
+          const uint32_t k0 = aK + ks * C::kPair, s0 = aS + (no & 1) * 16384;
+          const uint32_t lbo = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - k0;
 #pragma unroll
-        for (int s = 0; s < D / 16; ++s) {
-          const uint32_t off = (s >> 2) * C::kPairChunk + (s & 3) * 32;
-          const uint32_t offc = (s >> 2) * C::kCubeChunk + (s & 3) * 32;
-          umma_bf16(tbase + 128 + st * 64, make_sdesc_sw128(v0 + off, 16, 1024),
-                    make_sdesc_sw128(aO + offc, 16, 1024), idSD, s > 0);
+          for (int s = 0; s < 8; ++s)
+            umma_bf16(tbase + 256, make_sdesc_sw128(k0 + s * 2048, lbo, 1024),
+                      make_sdesc_sw128(s0 + s * 2048, 8192, 1024), idG, (no > 0 || s > 0) ? 1u : 0u);
+          umma_commit(&sm->k_empty[ks]);
+          umma_commit(&sm->d_empty[no & 1]);
+          ++no;
         }
-        umma_commit(&sm->v_empty[st]);
-        umma_commit(&sm->s_full[st]);
-      };
-      issue_SdP(0);
-      for (int p = 0; p < npairs; ++p) {
-        const int st = p & 1;
-        if (p + 1 < npairs) issue_SdP(p + 1);
-        mbar_wait(&sm->d_full[st], (p >> 1) & 1);
-        tc_fence_after();
-        const uint32_t k0 = aK + st * C::kPair, s0 = aS + st * 16384;
-        const uint32_t lbo = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - k0;
-#pragma unroll
-        for (int s = 0; s < 8; ++s)
-          umma_bf16(tbase + 256, make_sdesc_sw128(k0 + s * 2048, lbo, 1024), make_sdesc_sw128(s0 + s * 2048, 8192, 1024),
-                    idG, (p > 0 || s > 0) ? 1u : 0u);
-        umma_commit(&sm->k_empty[st]);
-        umma_commit(&sm->d_empty[st]);
       }
       umma_commit(&sm->final_bar);
     }
-  } else {  // warps 0-3: dS^T
-    const int kl = warp * 32 + lane;
-    const uint32_t lrow = tbase + (uint32_t(warp * 32) << 16);
-    for (int p = 0; p < npairs; ++p) {
-      const int st = p & 1;
-      const bool valid = kl < 64 || (2 * p + 1 < k_sel);
-      mbar_wait(&sm->s_full[st], (p >> 1) & 1);
+  } else if (warp < 8) {  // two warpgroups: dS^T
+    const int g = warp >> 2;
+    const int kl = (warp & 3) * 32 + lane;
+    const uint32_t lrow = tbase + (uint32_t((warp & 3) * 32) << 16);
+    uint8_t* dS = sS + g * 16384;
+    for (int p = g; p < npairs; p += 2) {
+      const bool valid = kl < 64 || (2 * p + 1 < k_sel);  // warp-uniform
+      mbar_wait(&sm->s_full[g], (p >> 1) & 1);
       tc_fence_after();
-      float s[64], dpv[64];
-      {
-        float t[32];
+      uint32_t pd[32];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          tmem_ld32(lrow + st * 64 + h * 32, t);
+      for (int h = 0; h < 2; ++h) {
+        uint32_t rs[32], rd[32];
+        tmem_ld32_raw(lrow + g * 64 + h * 32, rs);
+        tmem_ld32_raw(lrow + 128 + g * 64 + h * 32, rd);
+        tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) s[h * 32 + i] = t[i];
-          tmem_ld32(lrow + 128 + st * 64 + h * 32, t);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) dpv[h * 32 + i] = t[i];
+        for (int j = 0; j < 32; j += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(&sm->lse2[h * 32 + j]);
+          const float4 d4 = *reinterpret_cast<const float4*>(&sm->dl[h * 32 + j]);
+          const float p0 = ex2b(fmaf(__uint_as_float(rs[j]), scale_log2, -l4.x));
+          const float p1 = ex2b(fmaf(__uint_as_float(rs[j + 1]), scale_log2, -l4.y));
+          const float p2 = ex2b(fmaf(__uint_as_float(rs[j + 2]), scale_log2, -l4.z));
+          const float p3 = ex2b(fmaf(__uint_as_float(rs[j + 3]), scale_log2, -l4.w));
+          pd[h * 16 + j / 2] = pack_bf16(p0 * (__uint_as_float(rd[j]) - d4.x), p1 * (__uint_as_float(rd[j + 1]) - d4.y));
+          pd[h * 16 + j / 2 + 1] =
+              pack_bf16(p2 * (__uint_as_float(rd[j + 2]) - d4.z), p3 * (__uint_as_float(rd[j + 3]) - d4.w));
         }
       }
       tc_fence_before();
-      mbar_arrive(&sm->s_free[st]);
-      uint32_t pd[32];
+      mbar_arrive(&sm->s_free[g]);
+      if (!valid) {
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float4 l4 = *reinterpret_cast<const float4*>(&sm->lse2[2 * j]);
-        const float4 d4 = *reinterpret_cast<const float4*>(&sm->dl[2 * j]);
-        const float p0 = ex2b(fmaf(s[2 * j], scale_log2, -l4.x));
-        const float p1 = ex2b(fmaf(s[2 * j + 1], scale_log2, -l4.y));
-        const float p2 = ex2b(fmaf(s[2 * j + 2], scale_log2, -l4.z));
-        const float p3 = ex2b(fmaf(s[2 * j + 3], scale_log2, -l4.w));
-        pd[j] = valid ? pack_bf16(p0 * (dpv[2 * j] - d4.x), p1 * (dpv[2 * j + 1] - d4.y)) : 0u;
-        pd[j + 1] = valid ? pack_bf16(p2 * (dpv[2 * j + 2] - d4.z), p3 * (dpv[2 * j + 3] - d4.w)) : 0u;
+        for (int j = 0; j < 32; ++j) pd[j] = 0u;
       }
-      if (p >= 2) mbar_wait(&sm->d_empty[st], ((p >> 1) - 1) & 1);
-      uint8_t* dS = sS + st * 16384;
+      if (p >= 2) mbar_wait(&sm->d_empty[g], ((p >> 1) - 1) & 1);
 #pragma unroll
       for (int c = 0; c < 8; ++c)
         *reinterpret_cast<uint4*>(dS + sw128_offset(kl, c * 16)) =
             make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(&sm->d_full[st]);
+      mbar_arrive(&sm->d_full[g]);
     }
     // ---------------------------------------------------------------- epilogue
     mbar_wait(&sm->final_bar, 0);
     tc_fence_after();
     float* stQ = reinterpret_cast<float*>(sK);  // [64][D] fp32
-    if (kl < D) stage_transposed<D>(lrow + 256, stQ, kl, scale);
-    named_bar_b(1, 128);
-    write_rows<D>(L, u, qc, stQ, dqc, raster, dq, threadIdx.x, 128);
+    if (kl < D) stage_cols<D>(lrow + 256, g * 32, stQ, kl, scale);  // each warpgroup: 32 of the 64 q
+    named_bar_b(1, kCompute);
+    write_rows<D>(L, u, qc, stQ, dqc, raster, dq, threadIdx.x, kCompute);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 6) {
+  if (warp == 10) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }

@@ -197,34 +197,35 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
       const uint32_t lboV = (D == 128) ? uint32_t(C::kChunkStride) : smem_u32(sZ) - aV;
       mbar_wait(&sm->bar_q, 0);
-      auto issue_S = [&](int p) {
-        const int b = p & 1;
-        mbar_wait(&sm->k_full, p & 1);
-        if (p >= 2) mbar_wait(&sm->s_free[b], ((p >> 1) - 1) & 1);
-        tc_fence_after();
+      // Event-driven issue of two in-order streams: S(ns) = Kpair.Q^T and O(no) += V^T.P^T.
+      // Neither stream blocks the other (a blocking S(p+1) would serialise a TMA latency per pair).
+      int ns = 0, no = 0;
+      while (no < npairs) {
+        if (ns < npairs && mbar_try_wait(&sm->k_full, ns & 1) &&
+            (ns < 2 || mbar_try_wait(&sm->s_free[ns & 1], ((ns >> 1) - 1) & 1))) {
+          tc_fence_after();
 #pragma unroll
-        for (int s = 0; s < D / 16; ++s) {
-          const uint64_t a = make_sdesc_sw128(aK + (s >> 2) * C::kChunkStride + (s & 3) * 32, 16, 1024);
-          const uint64_t bq = make_sdesc_sw128(aQ + (s >> 2) * 8192 + (s & 3) * 32, 16, 1024);
-          umma_bf16(tbase + b * 64, a, bq, idS, s > 0);
+          for (int s = 0; s < D / 16; ++s) {
+            const uint64_t a = make_sdesc_sw128(aK + (s >> 2) * C::kChunkStride + (s & 3) * 32, 16, 1024);
+            const uint64_t bq = make_sdesc_sw128(aQ + (s >> 2) * 8192 + (s & 3) * 32, 16, 1024);
+            umma_bf16(tbase + (ns & 1) * 64, a, bq, idS, s > 0);
+          }
+          umma_commit(&sm->k_empty);
+          umma_commit(&sm->s_full[ns & 1]);
+          ++ns;
         }
-        umma_commit(&sm->k_empty);
-        umma_commit(&sm->s_full[b]);
-      };
-      issue_S(0);
-      for (int p = 0; p < npairs; ++p) {
-        if (p + 1 < npairs) issue_S(p + 1);
-        mbar_wait(&sm->p_full, p & 1);
-        mbar_wait(&sm->v_full, p & 1);
-        tc_fence_after();
+        if (no < ns && mbar_try_wait(&sm->p_full, no & 1) && mbar_try_wait(&sm->v_full, no & 1)) {
+          tc_fence_after();
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const uint64_t a = make_sdesc_sw128(aV + s * 2048, lboV, 1024);
-          const uint64_t bp = make_sdesc_sw128(aP + s * 2048, 8192, 1024);
-          umma_bf16(tbase + 128, a, bp, idO, (p > 0 || s > 0) ? 1u : 0u);
+          for (int s = 0; s < 8; ++s) {
+            const uint64_t a = make_sdesc_sw128(aV + s * 2048, lboV, 1024);
+            const uint64_t bp = make_sdesc_sw128(aP + s * 2048, 8192, 1024);
+            umma_bf16(tbase + 128, a, bp, idO, (no > 0 || s > 0) ? 1u : 0u);
+          }
+          umma_commit(&sm->v_empty);
+          umma_commit(&sm->p_empty);
+          ++no;
         }
-        umma_commit(&sm->v_empty);
-        umma_commit(&sm->p_empty);
       }
       umma_commit(&sm->o_final);
     }
