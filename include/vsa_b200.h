@@ -158,12 +158,17 @@ int vsa_coarse_backward(const vsa_layout_t* layout, int64_t bh, int64_t d, const
  *   coarse stage or vsa_selection_transpose. Deterministic (no atomics): dQ per
  *   query cube, dK/dV per key cube over the transposed map, q-cubes ascending.
  *   Unselected key cubes get exactly zero fine gradient (test_fine.cpp:149-169).
- * raster != 0 writes dq/dk/dv in raster order (padded rows dropped). */
+ * raster != 0 writes dq/dk/dv in raster order (padded rows dropped).
+ * workspace (device, >= vsa_fine_backward_workspace_bytes, may be NULL): with it the
+ * tcgen05 path stores the bf16 dS tiles from the dK/dV pass and computes dQ as a
+ * block-sparse GEMM over them (no S/dP recompute); without it dQ recomputes S and dP. */
 int vsa_fine_backward(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* q, const void* k,
                       const void* v, const void* dof, const float* lse, const float* delta, const int32_t* sel,
                       int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx, const float* dqc,
                       const float* dkc, const float* dvc, int32_t raster, int32_t flags, void* dq, void* dk,
-                      void* dv, void* stream);
+                      void* dv, void* workspace, size_t workspace_bytes, void* stream);
+/* Workspace size for the dS-materialising backward: B*H*nc*top_k tiles x (8 KiB + 4 B). */
+size_t vsa_fine_backward_workspace_bytes(const vsa_layout_t* layout, int64_t bh, int64_t top_k);
 
 /* Max-pool unpool (coarse.hpp:172-176): adds dxc[cube][j] to the first argmax
  * token of x (tiled) per (cube, channel) into dx (raster if `raster` else tiled, dtype). */

@@ -313,9 +313,11 @@ AttnGrads<Scalar> fine_backward(const TileLayout& layout, const AttnTensor<Scala
                                         nullptr));
   detail::check(vsa_backward_prologue(layout.raw(), bh, d, dt, 0, ddo.get(), ones.get(), nullptr, zoc.get(),
                                       dout_f.get(), 1, dof.get(), delta.get(), doc.get(), nullptr, nullptr, nullptr));
+  const size_t wsb = vsa_fine_backward_workspace_bytes(layout.raw(), bh, sel.k());
+  detail::DeviceBuffer<uint8_t> ws(wsb);
   detail::check(vsa_fine_backward(layout.raw(), bh, d, dt, dq_.get(), dk_.get(), dv_.get(), dof.get(), lse.get(),
                                   delta.get(), dsel.get(), sel.k(), offs.get(), idx.get(), nullptr, nullptr, nullptr, 0,
-                                  0, gq.get(), gk.get(), gv.get(), nullptr));
+                                  0, gq.get(), gk.get(), gv.get(), ws.get(), wsb, nullptr));
   AttnGrads<Scalar> g{AttnTensor<Scalar>(q.batch(), q.heads(), q.seq(), d),
                       AttnTensor<Scalar>(q.batch(), q.heads(), q.seq(), d),
                       AttnTensor<Scalar>(q.batch(), q.heads(), q.seq(), d)};

@@ -31,7 +31,7 @@ EXPORTS = [
     "vsa_last_error", "vsa_version", "vsa_kernel_launches", "vsa_layout_make", "vsa_flatten_index", "vsa_tile", "vsa_untile",
     "vsa_tile_pool", "vsa_pool_tiled", "vsa_coarse_forward", "vsa_coarse_bitmap_bytes", "vsa_selection_transpose",
     "vsa_validate_selection", "vsa_fine_forward", "vsa_backward_prologue", "vsa_coarse_backward",
-    "vsa_fine_backward", "vsa_unpool_max_add",
+    "vsa_fine_backward", "vsa_fine_backward_workspace_bytes", "vsa_unpool_max_add",
 ]
 
 
@@ -76,7 +76,8 @@ def lib():
         "vsa_fine_forward": [LP, I64, I64, I32, P, P, P, P, I64, P, P, P, P, P, P, I32, P, P],
         "vsa_backward_prologue": [LP, I64, I64, I32, I32, P, P, P, P, P, I32, P, P, P, P, P, P],
         "vsa_coarse_backward": [LP, I64, I64, P, P, P, P, P, P, P, P, P, P],
-        "vsa_fine_backward": [LP, I64, I64, I32, P, P, P, P, P, P, P, I64, P, P, P, P, P, I32, I32, P, P, P, P],
+        "vsa_fine_backward": [LP, I64, I64, I32, P, P, P, P, P, P, P, I64, P, P, P, P, P, I32, I32, P, P, P, P,
+                              C.c_size_t, P],
         "vsa_unpool_max_add": [LP, I64, I64, I32, P, P, I32, P, P],
     }
     for name, args in sig.items():
@@ -85,6 +86,8 @@ def lib():
         f.restype = C.c_int
     L.vsa_coarse_bitmap_bytes.argtypes = [LP, I64]
     L.vsa_coarse_bitmap_bytes.restype = C.c_size_t
+    L.vsa_fine_backward_workspace_bytes.argtypes = [LP, I64, I64]
+    L.vsa_fine_backward_workspace_bytes.restype = C.c_size_t
     _lib = L
     return L
 

@@ -290,10 +290,12 @@ def fine_forward(layout: TileLayout, q, k, v, sel, force_simt: bool = False) -> 
     return FineResult(out, rmax, lse)
 
 
-def fine_backward(layout: TileLayout, q, k, v, sel, dout, row_lse, out=None, selT=None, force_simt=False):
+def fine_backward(layout: TileLayout, q, k, v, sel, dout, row_lse, out=None, selT=None, force_simt=False,
+                  workspace=True):
     """fine_backward (fine.hpp:107-204) -> tiled (dq, dk, dv). `out` (the forward
     output) lets delta be read as rowsum(dO*O); without it delta is recomputed
-    by one extra pass."""
+    by one extra pass. `workspace=True` uses the dS-materialising path (dQ as a
+    GEMM over stored dS tiles); False recomputes S and dP for dQ."""
     _check_fine(layout, q, k, v, sel)
     if dout.shape != q.shape:
         raise ValueError("fine_backward: dO shape mismatch")
@@ -313,9 +315,11 @@ def fine_backward(layout: TileLayout, q, k, v, sel, dout, row_lse, out=None, sel
                                         _p(out), 1, _p(dof), _p(delta), _p(doc), None, None, _stream()))
     dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
     flags = L.FINE_FORCE_SIMT if force_simt else 0
+    wsb = L.lib().vsa_fine_backward_workspace_bytes(layout.ref(), B * H, sel.shape[3])
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=q.device) if workspace else None
     check(L.lib().vsa_fine_backward(layout.ref(), B * H, d, _dt(q), _p(q), _p(k), _p(v), _p(dof), _p(row_lse),
                                     _p(delta), _p(sel), sel.shape[3], _p(offs), _p(idx), None, None, None, 0, flags,
-                                    _p(dq), _p(dk), _p(dv), _stream()))
+                                    _p(dq), _p(dk), _p(dv), _p(ws), wsb if workspace else 0, _stream()))
     return dq, dk, dv
 
 
@@ -332,12 +336,15 @@ class VsaOp:
 
     def __init__(self, layout: TileLayout, B: int, H: int, d: int, top_k: int, dtype=torch.bfloat16,
                  pool: int = POOL_MEAN, adaptation: bool = False, raster: bool = True, device="cuda",
-                 force_simt: bool = False):
+                 force_simt: bool = False, bwd_workspace: bool = True):
         if not (1 <= top_k <= layout.num_cubes):
             raise ValueError("coarse_forward_select: k must be in [1, num_cubes]")
         self.layout, self.B, self.H, self.d, self.top_k = layout, B, H, d, int(top_k)
         self.dtype, self.pool, self.adaptation, self.raster = dtype, pool, adaptation, raster
         self.force_simt = force_simt
+        # dS-materialising backward workspace (B*H*nc*k bf16 64x64 tiles), allocated on first backward
+        self.bwd_workspace = bwd_workspace
+        self.ws = None
         nc, Lp = layout.num_cubes, layout.seq_padded
         e = lambda *s, dt=dtype: torch.empty(s, dtype=dt, device=device)
         f32, i32 = torch.float32, torch.int32
@@ -463,10 +470,14 @@ class VsaOp:
         mean = self.pool == POOL_MEAN
         qt, kt, vt = self._qkv
         flags = L.FINE_FORCE_SIMT if self.force_simt else 0
+        wsb = lib.vsa_fine_backward_workspace_bytes(lr, bh, self.fine_k) if self.bwd_workspace else 0
+        if wsb and (self.ws is None or self.ws.numel() < wsb):
+            self.ws = torch.empty(wsb, dtype=torch.uint8, device=dout.device)
         check(lib.vsa_fine_backward(lr, bh, d, dt, _p(qt), _p(kt), _p(vt), _p(self.dof), _p(self.lse),
                                     _p(self.delta), _p(self.fine_sel), self.fine_k, _p(self.selT_offs),
                                     _p(self.selT_idx), _p(self.dqc) if mean else None, _p(self.dkc) if mean else None,
-                                    _p(self.dvc) if mean else None, raster, flags, _p(dq), _p(dk), _p(dv), st))
+                                    _p(self.dvc) if mean else None, raster, flags, _p(dq), _p(dk), _p(dv),
+                                    _p(self.ws) if wsb else None, wsb, st))
         self._mark("fine_bwd")
         if not mean:
             for x, dc, g in ((qt, self.dqc, dq), (kt, self.dkc, dk), (vt, self.dvc, dv)):

@@ -232,7 +232,7 @@ int vsa_fine_backward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtyp
                       const void* v, const void* dof, const float* lse, const float* delta, const int32_t* sel,
                       int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx, const float* dqc,
                       const float* dkc, const float* dvc, int32_t raster, int32_t flags, void* dq, void* dk,
-                      void* dv, void* stream) {
+                      void* dv, void* workspace, size_t workspace_bytes, void* stream) {
   VSA_CHECKED(check_layout(L));
   VSA_REQUIRE(dtype_ok(dtype), "fine_backward: unknown dtype");
   VSA_REQUIRE(q && k && v && dof && sel && dq && dk && dv && bh >= 1, "fine_backward: null buffer");
@@ -243,9 +243,14 @@ int vsa_fine_backward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtyp
   cudaStream_t st = as_stream(stream);
   if (!(flags & VSA_FINE_FORCE_SIMT) && sm100_fine_bwd_supported(*L, d, dtype))
     return launch_fine_backward_sm100(*L, bh, d, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc,
-                                      dvc, raster, dq, dk, dv, st);
+                                      dvc, raster, dq, dk, dv, workspace, workspace_bytes, st);
   return launch_fine_backward_simt(*L, bh, d, dtype, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc,
                                    dkc, dvc, raster, dq, dk, dv, st);
+}
+
+size_t vsa_fine_backward_workspace_bytes(const vsa_layout_t* L, int64_t bh, int64_t top_k) {
+  if (!L || bh < 1 || top_k < 1) return 0;
+  return fine_backward_ws_bytes(*L, bh, top_k);
 }
 
 int vsa_unpool_max_add(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled,

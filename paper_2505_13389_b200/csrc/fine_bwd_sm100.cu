@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                            const float* __restrict__ delta, const int32_t* __restrict__ offs,
                            const int32_t* __restrict__ idx, const float* __restrict__ dkc,
                            const float* __restrict__ dvc, int raster, __nv_bfloat16* __restrict__ dk,
-                           __nv_bfloat16* __restrict__ dv) {
+                           __nv_bfloat16* __restrict__ dv, const __grid_constant__ CUtensorMap tm_ds,
+                           const int32_t* __restrict__ ds_pos, int ds_store) {
   using C = KVCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
@@ -218,8 +219,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // Event-driven issue of two in-order streams: {S, dP}(ns) and {dV, dK}(no).
       int ns = 0, no = 0;
       while (no < npairs) {
-        if (ns < npairs && mbar_try_wait(&sm->q_full[ns & 1], (ns >> 1) & 1) &&
-            (ns < 2 || mbar_try_wait(&sm->s_free[ns & 1], ((ns >> 1) - 1) & 1))) {
+        if (ns < npairs && mbar_test_wait(&sm->q_full[ns & 1], (ns >> 1) & 1) &&
+            (ns < 2 || mbar_test_wait(&sm->s_free[ns & 1], ((ns >> 1) - 1) & 1))) {
           const int st = ns & 1;
           tc_fence_after();
           const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           umma_commit(&sm->s_full[st]);
           ++ns;
         }
-        if (no < ns && mbar_try_wait(&sm->pd_full[no & 1], (no >> 1) & 1)) {
+        if (no < ns && mbar_test_wait(&sm->pd_full[no & 1], (no >> 1) & 1)) {
           const int st = no & 1;
           tc_fence_after();
           const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
@@ -295,7 +296,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) pp[j] = pd[j] = 0u;
       }
-      if (p >= 2) mbar_wait(&sm->pd_empty[g], ((p >> 1) - 1) & 1);
+      if (p >= 2) {
+        mbar_wait(&sm->pd_empty[g], ((p >> 1) - 1) & 1);
+        if (ds_store && ql == 0) bulk_wait_group_read0();  // previous dS tile store has read myS
+        named_bar_b(2 + g, 128);
+      }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         *reinterpret_cast<uint4*>(myP + sw128_offset(ql, c * 16)) =
@@ -304,9 +309,24 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
       }
       fence_proxy_async_smem();
+      if (ds_store) {
+        // materialise the bf16 dS tiles [64 q][64 keys] for the dQ GEMM: tile (qcube, t) at
+        // rows ((u*nc + qcube)*k + t)*64 of the dS store, t = position of kc in sel[qcube]
+        named_bar_b(2 + g, 128);
+        if (ql == 0) {
+          const int64_t base = u * int64_t(L.nc) * k_sel;
+          const int e = beg + 2 * p;
+          tma_store_2d(&tm_ds, myS, 0, int((base + int64_t(list[e]) * k_sel + ds_pos[base + e]) * 64));
+          if (2 * p + 1 < nq)
+            tma_store_2d(&tm_ds, myS + 8192, 0,
+                         int((base + int64_t(list[e + 1]) * k_sel + ds_pos[base + e + 1]) * 64));
+          bulk_commit_group();
+        }
+      }
       tc_fence_before();
       mbar_arrive(&sm->pd_full[g]);
     }
+    if (ds_store && ql == 0) bulk_wait_group0();
     // ---------------------------------------------------------------- epilogue
     float* stK = reinterpret_cast<float*>(sQ);                 // [64][D] fp32
     float* stV = reinterpret_cast<float*>(sQ + 64 * D * 4);    // [64][D] fp32
@@ -330,7 +350,155 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
 }
 
-// ============================================================================ dQ
+// ============================================================================ dQ from stored dS
+// dQ^T[d x 64 q] += Kpair^T . dS^T over the selected pairs, with the bf16 dS tiles
+// written by the dK/dV kernel: a pure block-sparse GEMM (no S/dP recompute, no exp).
+//   A = Kpair MN-major (the K-major TMA tile read transposed), B = dS^T = the stored
+//   [64 q][64 keys] tiles, K-major, one 64-key chunk per tile of the pair.
+// 2 CTAs/SM (one epilogue overlaps the other's stream), 2-stage {Kpair, dS pair} ring.
+constexpr int kDQThreads = 192;
+
+template <int D>
+struct DQCfg {
+  static constexpr int kChunks = D / 64;
+  static constexpr int kPair = 128 * D * 2;
+  static constexpr int kStage = kPair + 16384;
+  static constexpr int kStages = 2;
+  static constexpr int kOffZ = kStages * kStage;
+  static constexpr int kTiles = kOffZ + (D == 64 ? 16384 : 0);
+  static constexpr int kPairChunk = 16384;
+};
+
+struct DQSmall {
+  uint64_t full[2], empty[2], final_bar;
+  uint32_t tmem;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kDQThreads, 2)
+    fine_dq_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_ds,
+                              DevLayout L, int k_sel, float scale, const int32_t* __restrict__ sel,
+                              const float* __restrict__ dqc, int raster, __nv_bfloat16* __restrict__ dq) {
+  using C = DQCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  uint8_t* sZ = smem + C::kOffZ;
+  DQSmall* sm = reinterpret_cast<DQSmall*>(smem + C::kTiles);
+  const int warp = int(warp_id()), lane = int(lane_id());
+  const int qc = blockIdx.x;
+  const int64_t u = blockIdx.y;
+  const int npairs = (k_sel + 1) >> 1;
+  const int32_t* srow = sel + (u * L.nc + qc) * int64_t(k_sel);
+  const int row0 = int(u * L.seqp);
+  const int64_t ds_row0 = (u * L.nc + qc) * int64_t(k_sel) * 64;
+
+  if (warp == 5) tmem_alloc<64>(&sm->tmem);
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < C::kStages; ++b) {
+      mbar_init(&sm->full[b], 1);
+      mbar_init(&sm->empty[b], 1);
+    }
+    mbar_init(&sm->final_bar, 1);
+    fence_barrier_init();
+  }
+  if (D == 64)
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) reinterpret_cast<uint4*>(sZ)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = sm->tmem;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_ds);
+      for (int p = 0; p < npairs; ++p) {
+        const int st = p % C::kStages;
+        const bool hb = 2 * p + 1 < k_sel;
+        uint8_t* sK = smem + st * C::kStage;
+        uint8_t* sD = sK + C::kPair;
+        mbar_wait(&sm->empty[st], ((p / C::kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm->full[st], (hb ? 2 : 1) * (64 * D * 2 + 8192));
+        const int ka = srow[2 * p];
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_2d(sK + c * C::kPairChunk, &tm_k, &sm->full[st], c * 64, row0 + ka * 64);
+        tma_load_2d(sD, &tm_ds, &sm->full[st], 0, int(ds_row0 + int64_t(2 * p) * 64));
+        if (hb) {
+          const int kb = srow[2 * p + 1];
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_2d(sK + c * C::kPairChunk + 8192, &tm_k, &sm->full[st], c * 64, row0 + kb * 64);
+          tma_load_2d(sD + 8192, &tm_ds, &sm->full[st], 0, int(ds_row0 + int64_t(2 * p + 1) * 64));
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      const uint32_t idG = make_idesc_bf16(128, 64, true, false);  // A MN-major, B K-major
+      for (int p = 0; p < npairs; ++p) {
+        const int st = p % C::kStages;
+        const bool hb = 2 * p + 1 < k_sel;
+        mbar_wait(&sm->full[st], (p / C::kStages) & 1);
+        tc_fence_after();
+        const uint32_t k0 = smem_u32(smem + st * C::kStage), d0 = k0 + C::kPair;
+        const uint32_t lbo = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - k0;
+        const int nsteps = hb ? 8 : 4;  // a single-cube last pair contributes 64 keys
+        for (int s = 0; s < nsteps; ++s)
+          umma_bf16(tbase, make_sdesc_sw128(k0 + s * 2048, lbo, 1024),
+                    make_sdesc_sw128(d0 + (s >> 2) * 8192 + (s & 3) * 32, 16, 1024), idG, (p > 0 || s > 0) ? 1u : 0u);
+        umma_commit(&sm->empty[st]);
+      }
+      umma_commit(&sm->final_bar);
+    }
+  } else if (warp < 4) {
+    const int dl = warp * 32 + lane;
+    const uint32_t lrow = tbase + (uint32_t(warp * 32) << 16);
+    mbar_wait(&sm->final_bar, 0);
+    tc_fence_after();
+    float* st = reinterpret_cast<float*>(smem);  // [64][D] fp32 over the (now idle) stages
+    if (dl < D) {
+      stage_cols<D>(lrow, 0, st, dl, scale);
+      stage_cols<D>(lrow, 32, st, dl, scale);
+    }
+    named_bar_b(1, 128);
+    write_rows<D>(L, u, qc, st, dqc, raster, dq, threadIdx.x, 128);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<64>(tbase);
+  }
+}
+
+// Position of each transposed-map entry's key cube inside its query cube's sel row
+// (the `t` of dS tile (qcube, t)). One thread per CSR entry; two binary searches.
+__global__ void selT_positions_kernel(int64_t bh, int nc, int k, const int32_t* __restrict__ sel,
+                                      const int32_t* __restrict__ offs, const int32_t* __restrict__ idx,
+                                      int32_t* __restrict__ pos) {
+  const int64_t per = int64_t(nc) * k;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < bh * per; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t u = e / per;
+    const int i = int(e - u * per);
+    const int32_t* o = offs + u * (nc + 1);
+    int lo = 0, hi = nc;  // kc = last index with o[kc] <= i
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (o[mid] <= i) lo = mid; else hi = mid;
+    }
+    const int kc = lo;
+    const int qcube = idx[u * per + i];
+    const int32_t* r = sel + (u * nc + qcube) * int64_t(k);
+    int a = 0, b = k;  // lower_bound of kc in the ascending row
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (r[mid] < kc) a = mid + 1; else b = mid;
+    }
+    pos[u * per + i] = a;
+  }
+}
+
+// ============================================================================ dQ (recompute variant)
 template <int D>
 struct QCfg {
   static constexpr int kChunks = D / 64;
@@ -471,8 +639,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       while (no < npairs) {
         if (ns < npairs) {
           const int st = ns & 1, ks = ns % C::kKStages;
-          if ((ns < 2 || mbar_try_wait(&sm->s_free[st], ((ns >> 1) - 1) & 1)) &&
-              mbar_try_wait(&sm->k_full[ks], (ns / C::kKStages) & 1) && mbar_try_wait(&sm->v_full[st], (ns >> 1) & 1)) {
+          if ((ns < 2 || mbar_test_wait(&sm->s_free[st], ((ns >> 1) - 1) & 1)) &&
+              mbar_test_wait(&sm->k_full[ks], (ns / C::kKStages) & 1) && mbar_test_wait(&sm->v_full[st], (ns >> 1) & 1)) {
             tc_fence_after();
             const uint32_t k0 = aK + ks * C::kPair, v0 = aV + st * C::kPair;
 #pragma unroll
@@ -489,7 +657,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             ++ns;
           }
         }
-        if (no < ns && mbar_try_wait(&sm->d_full[no & 1], (no >> 1) & 1)) {
+        if (no < ns && mbar_test_wait(&sm->d_full[no & 1], (no >> 1) & 1)) {
           tc_fence_after();
           const int ks = no % C::kKStages;
           const uint32_t k0 = aK + ks * C::kPair, s0 = aS + (no & 1) * 16384;
@@ -578,19 +746,34 @@ template <int D>
 static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const void* k, const void* v,
                       const void* dof, const float* lse, const float* delta, const int32_t* sel, int64_t top_k,
                       const int32_t* offs, const int32_t* idx, const float* dqc, const float* dkc, const float* dvc,
-                      int32_t raster, void* dq, void* dk, void* dv, cudaStream_t st) {
-  CUtensorMap tq, tk, tv, tdo;
+                      int32_t raster, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, cudaStream_t st) {
+  CUtensorMap tq, tk, tv, tdo, tds;
   const uint64_t rows = uint64_t(bh * Lh.seq_padded);
   if (!make_tmap_bf16_sw128(&tq, q, rows, D, 64) || !make_tmap_bf16_sw128(&tk, k, rows, D, 64) ||
       !make_tmap_bf16_sw128(&tv, v, rows, D, 64) || !make_tmap_bf16_sw128(&tdo, dof, rows, D, 64)) {
     set_error("fine_backward: cuTensorMapEncodeTiled failed");
     return VSA_EINVAL;
   }
+  // dS materialisation needs the workspace (bf16 tiles + CSR positions); without it
+  // dQ recomputes S and dP (the fallback kernel).
+  const bool store_ds = ws != nullptr && ws_bytes >= fine_backward_ws_bytes(Lh, bh, top_k);
+  const int64_t tiles = bh * Lh.nc * top_k;
+  int32_t* pos = store_ds ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + tiles * 8192) : nullptr;
+  if (store_ds && !make_tmap_bf16_sw128(&tds, ws, uint64_t(tiles) * 64, 64, 64)) {
+    set_error("fine_backward: cuTensorMapEncodeTiled (dS) failed");
+    return VSA_EINVAL;
+  }
+  if (!store_ds) tds = tq;  // unused
   const float scale = 1.0f / std::sqrt(float(D));
   const float scale_log2 = scale * 1.4426950408889634f;
   const DevLayout L = to_dev(Lh);
   dim3 grid(unsigned(Lh.nc), unsigned(bh));
-  {
+  if (store_ds) {
+    const int blocks = int(std::min<int64_t>((tiles + 255) / 256, 148 * 8));
+    selT_positions_kernel<<<blocks, 256, 0, st>>>(bh, int(Lh.nc), int(top_k), sel, offs, idx, pos);
+    int rc = kernel_status("selT_positions_kernel");
+    if (rc) return rc;
+  } else {
     const size_t smem = QCfg<D>::kTiles + sizeof(QSmall) + 1024;
     auto kern = fine_dq_sm100_kernel<D>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -605,21 +788,36 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     kern<<<grid, kBwdThreads, smem, st>>>(tq, tk, tv, tdo, L, int(top_k), scale, scale_log2, lse, delta, offs, idx,
                                          dkc, dvc, raster, static_cast<__nv_bfloat16*>(dk),
-                                         static_cast<__nv_bfloat16*>(dv));
+                                         static_cast<__nv_bfloat16*>(dv), tds, pos, store_ds ? 1 : 0);
+    int rc = kernel_status("fine_dkdv_sm100_kernel");
+    if (rc) return rc;
   }
-  VSA_LAUNCH_CHECK("fine_dkdv_sm100_kernel");
+  if (store_ds) {
+    const size_t smem = DQCfg<D>::kTiles + sizeof(DQSmall) + 1024;
+    auto kern = fine_dq_gemm_sm100_kernel<D>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kern<<<grid, kDQThreads, smem, st>>>(tk, tds, L, int(top_k), scale, sel, dqc, raster,
+                                        static_cast<__nv_bfloat16*>(dq));
+    return kernel_status("fine_dq_gemm_sm100_kernel");
+  }
+  return 0;
+}
+
+size_t fine_backward_ws_bytes(const vsa_layout_t& L, int64_t bh, int64_t top_k) {
+  const int64_t tiles = bh * L.nc * top_k;
+  return size_t(tiles) * (8192 + 4);
 }
 
 int launch_fine_backward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, const void* q, const void* k,
                                const void* v, const void* dof, const float* lse, const float* delta,
                                const int32_t* sel, int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx,
                                const float* dqc, const float* dkc, const float* dvc, int32_t raster, void* dq,
-                               void* dk, void* dv, cudaStream_t st) {
+                               void* dk, void* dv, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (d == 128)
     return bwd_launch<128>(L, bh, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc, dvc, raster,
-                           dq, dk, dv, st);
+                           dq, dk, dv, ws, ws_bytes, st);
   return bwd_launch<64>(L, bh, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc, dvc, raster, dq,
-                        dk, dv, st);
+                        dk, dv, ws, ws_bytes, st);
 }
 
 }  // namespace vsa_host

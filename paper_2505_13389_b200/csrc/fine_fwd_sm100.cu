@@ -201,8 +201,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       // Neither stream blocks the other (a blocking S(p+1) would serialise a TMA latency per pair).
       int ns = 0, no = 0;
       while (no < npairs) {
-        if (ns < npairs && mbar_try_wait(&sm->k_full, ns & 1) &&
-            (ns < 2 || mbar_try_wait(&sm->s_free[ns & 1], ((ns >> 1) - 1) & 1))) {
+        if (ns < npairs && mbar_test_wait(&sm->k_full, ns & 1) &&
+            (ns < 2 || mbar_test_wait(&sm->s_free[ns & 1], ((ns >> 1) - 1) & 1))) {
           tc_fence_after();
 #pragma unroll
           for (int s = 0; s < D / 16; ++s) {
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
           umma_commit(&sm->s_full[ns & 1]);
           ++ns;
         }
-        if (no < ns && mbar_try_wait(&sm->p_full, no & 1) && mbar_try_wait(&sm->v_full, no & 1)) {
+        if (no < ns && mbar_test_wait(&sm->p_full, no & 1) && mbar_test_wait(&sm->v_full, no & 1)) {
           tc_fence_after();
 #pragma unroll
           for (int s = 0; s < 8; ++s) {

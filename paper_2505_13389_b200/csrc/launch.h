@@ -59,6 +59,7 @@ int launch_fine_backward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, con
                                const void* v, const void* dof, const float* lse, const float* delta,
                                const int32_t* sel, int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx,
                                const float* dqc, const float* dkc, const float* dvc, int32_t raster, void* dq,
-                               void* dk, void* dv, cudaStream_t st);
+                               void* dk, void* dv, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t fine_backward_ws_bytes(const vsa_layout_t& L, int64_t bh, int64_t top_k);
 
 }  // namespace vsa_host

@@ -116,6 +116,10 @@ def test_fine_forward_backward(vsa, cfg, dtype):
     g = vsa.fine_backward(L, dq_, dk_, dv_, dsel, do_, res.row_lse, out=res.out)
     for got, ref, n in zip(g, (fdq, fdk, fdv), ("dq", "dk", "dv")):
         assert_close(host(got), ref, dtype, n)
+    # the recompute-dQ variant (no dS workspace) agrees as well
+    g2 = vsa.fine_backward(L, dq_, dk_, dv_, dsel, do_, res.row_lse, out=res.out, workspace=False)
+    for got, ref, n in zip(g2, (fdq, fdk, fdv), ("dq", "dk", "dv")):
+        assert_close(host(got), ref, dtype, n + " (recompute)")
     # unselected key cubes: exactly zero dK/dV (test_fine.cpp:149-169)
     used = np.zeros((p.B, p.H, L.num_cubes), bool)
     for b in range(p.B):
