@@ -240,18 +240,16 @@ def run_ours(args, rank, world, local_rank):
                      speedup_vsa_vs_dense=round(dms / ms, 2))
         del opd
 
-    # e2e through the public API with pinned host buffers
+    # e2e through the public API with pinned host buffers: VsaHostPipeline overlaps the
+    # H2D of unit-group i+1 and the D2H of group i-1 with the kernels of group i
     hin = [t.cpu().pin_memory() for t in (q, k, v, gc, gf, do)]
     hout = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
-    din = [torch.empty_like(t) for t in (q, k, v, gc, gf, do)]
+    del op  # free the resident-input operator's buffers before building the pipeline
+    torch.cuda.empty_cache()
+    pipe = vsa.VsaHostPipeline(L, cfg["B"], cfg["H"], d, K, chunks=args.e2e_chunks, dtype=dtype)
 
     def e2e_step():
-        for dst, src in zip(din, hin):
-            dst.copy_(src, non_blocking=True)
-        op.forward(*din[:5], out=outs[0])
-        op.backward(din[5], *outs[1:])
-        for dst, src in zip(hout, outs):
-            dst.copy_(src, non_blocking=True)
+        pipe.run(hin, hout)
 
     e2e_step()
     barrier()
@@ -397,6 +395,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="host-pipeline unit groups for the e2e leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -6,7 +6,8 @@ The six sm_100a kernels live in ``csrc/`` behind the C ABI ``include/vsa_b200.h`
 """
 from ._lib import LIB_PATH, VsaError, build, lib  # noqa: F401
 from .api import (  # noqa: F401
-    POOL_MAX, POOL_MEAN, CoarseArtifacts, FineResult, TileLayout, VsaOp, VsaParams, all_cubes, coarse_backward,
+    POOL_MAX, POOL_MEAN, CoarseArtifacts, FineResult, TileLayout, VsaHostPipeline, VsaOp, VsaParams, all_cubes,
+    coarse_backward,
     coarse_forward_select, coarse_from_pooled, fine_backward, fine_forward, flatten_index, gate_backward,
     gates_from_hidden, pool_cubes, selection_transpose, tile, tile_pool, untile, validate_selection,
 )

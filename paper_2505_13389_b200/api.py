@@ -492,6 +492,75 @@ class VsaOp:
                                self.pool, self.layout.cube_size)
 
 
+class VsaHostPipeline:
+    """Forward + backward on HOST (pinned) tensors with the H2D / D2H copies
+    overlapped with the kernels.
+
+    Every (b, h) unit is independent (fine.hpp:65,129,172), so the B*H units are
+    split into `chunks` groups; group i+1 is copied in on one stream while group
+    i computes, and group i-1 is copied out on a third — double-buffered device
+    inputs/outputs, events for the hand-offs. Result == VsaOp on the whole batch.
+    """
+
+    def __init__(self, layout: TileLayout, B: int, H: int, d: int, top_k: int, chunks: int = 4,
+                 dtype=torch.bfloat16, device="cuda", **op_kwargs):
+        units = B * H
+        chunks = max(1, min(chunks, units))
+        self.bounds = [(units * i) // chunks for i in range(chunks + 1)]
+        self.units, self.d, self.S, self.dtype = units, d, layout.seq_len, dtype
+        cmax = max(b - a for a, b in zip(self.bounds[:-1], self.bounds[1:]))
+        self.ops = [VsaOp(layout, 1, cmax, d, top_k, dtype=dtype, device=device, **op_kwargs) for _ in range(2)]
+        e = lambda: torch.empty((1, cmax, self.S, d), dtype=dtype, device=device)
+        self.din = [[e() for _ in range(6)] for _ in range(2)]
+        self.dout = [[e() for _ in range(6)] for _ in range(2)]
+        self.s_in, self.s_out = torch.cuda.Stream(device), torch.cuda.Stream(device)
+        self.h2d_bytes = 6 * units * self.S * d * torch.tensor([], dtype=dtype).element_size()
+        self.d2h_bytes = self.h2d_bytes
+
+    def run(self, hin, hout):
+        """hin = (q, k, v, gc, gf, dO), hout = (O, dQ, dK, dV, dGc, dGf): pinned host [B,H,S,d]."""
+        flat = lambda t: t.view(self.units, self.S, self.d)
+        hin, hout = [flat(t) for t in hin], [flat(t) for t in hout]
+        comp = torch.cuda.current_stream()
+        n = len(self.bounds) - 1
+        ev_in, ev_comp, ev_out = [None] * n, [None] * n, [None] * n
+        for i in range(n):
+            a, b = self.bounds[i], self.bounds[i + 1]
+            c, slot = b - a, i % 2
+            with torch.cuda.stream(self.s_in):
+                if i >= 2:
+                    self.s_in.wait_event(ev_comp[i - 2])      # slot's inputs consumed
+                for dst, src in zip(self.din[slot], hin):
+                    dst[0, :c].copy_(src[a:b], non_blocking=True)
+                ev_in[i] = torch.cuda.Event()
+                ev_in[i].record(self.s_in)
+            comp.wait_event(ev_in[i])
+            if i >= 2:
+                comp.wait_event(ev_out[i - 2])                # slot's outputs drained
+            op, di, do = self.ops[slot], self.din[slot], self.dout[slot]
+            if c == op.H:
+                op.forward(*di[:5], out=do[0], check_inputs=False)
+                op.backward(di[5], *do[1:], check_inputs=False)
+            else:  # ragged last group: run on views of the right head count
+                sub = VsaOp(op.layout, 1, c, self.d, op.top_k, dtype=self.dtype, device=di[0].device)
+                v = lambda t: t[:, :c].contiguous()
+                o = sub.forward(*(v(t) for t in di[:5]))
+                g = sub.backward(v(di[5]))
+                for dst, src in zip(do, (o, *g)):
+                    dst[:, :c].copy_(src)
+            ev_comp[i] = torch.cuda.Event()
+            ev_comp[i].record(comp)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(ev_comp[i])
+                for dst, src in zip(hout, do):
+                    dst[a:b].copy_(src[0, :c], non_blocking=True)
+                ev_out[i] = torch.cuda.Event()
+                ev_out[i].record(self.s_out)
+        comp.wait_event(ev_out[n - 1])
+        if n >= 2:
+            comp.wait_event(ev_out[n - 2])
+
+
 # ----------------------------------------------------------------------------- gate projection (vsa.hpp:100-112)
 @dataclass
 class VsaParams:
