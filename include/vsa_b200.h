@@ -65,6 +65,10 @@ const char* vsa_last_error(void);
 const char* vsa_version(void);
 /* Number of CUDA kernels this library has launched in this process (all entries). */
 uint64_t vsa_kernel_launches(void);
+/* Debug: record pipeline events (clock64, code, index) of CTA (cta_x, cta_y) of the
+ * instrumented kernels into the device buffer `buf` (uint64: [0] = count, then pairs);
+ * buf = NULL disables. Not thread-safe; for profiling only. */
+int vsa_debug_trace(void* buf, int32_t cap, int32_t cta_x, int32_t cta_y);
 
 /* Replaces: TileLayout::TileLayout (layout.cpp:6-31). VSA_PAD_REJECT reproduces
  * the reference's divisibility check (layout.cpp:10-11); VSA_PAD_ZERO rounds the

@@ -28,7 +28,7 @@ class vsa_layout_t(C.Structure):
 
 
 EXPORTS = [
-    "vsa_last_error", "vsa_version", "vsa_kernel_launches", "vsa_layout_make", "vsa_flatten_index", "vsa_tile", "vsa_untile",
+    "vsa_last_error", "vsa_version", "vsa_kernel_launches", "vsa_debug_trace", "vsa_layout_make", "vsa_flatten_index", "vsa_tile", "vsa_untile",
     "vsa_tile_pool", "vsa_pool_tiled", "vsa_coarse_forward", "vsa_coarse_bitmap_bytes", "vsa_selection_transpose",
     "vsa_validate_selection", "vsa_fine_forward", "vsa_backward_prologue", "vsa_coarse_backward",
     "vsa_fine_backward", "vsa_fine_backward_workspace_bytes", "vsa_unpool_max_add",
@@ -65,6 +65,7 @@ def lib():
     L.vsa_kernel_launches.restype = C.c_uint64
     sig = {
         "vsa_layout_make": [I64] * 6 + [I32, LP],
+        "vsa_debug_trace": [P, I32, I32, I32],
         "vsa_flatten_index": [LP, I64, I64, I64, C.POINTER(I64)],
         "vsa_tile": [LP, I64, I64, I32, P, P, P],
         "vsa_untile": [LP, I64, I64, I32, P, P, P],

@@ -31,6 +31,9 @@ int cuda_status(cudaError_t e, const char* where) {
 }
 
 static std::atomic<uint64_t> g_launches{0};
+static vsa_dev::TraceCfg g_trace{nullptr, 0, 0, 0};
+
+vsa_dev::TraceCfg debug_trace() { return g_trace; }
 
 int kernel_status(const char* where) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -71,6 +74,11 @@ extern "C" {
 const char* vsa_last_error(void) { return g_err.c_str(); }
 const char* vsa_version(void) { return "vsa_b200 0.1 (sm_100a)"; }
 uint64_t vsa_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int vsa_debug_trace(void* buf, int32_t cap, int32_t cta_x, int32_t cta_y) {
+  g_trace = vsa_dev::TraceCfg{static_cast<unsigned long long*>(buf), cap, cta_x, cta_y};
+  return VSA_OK;
+}
 
 int vsa_layout_make(int64_t t, int64_t h, int64_t w, int64_t ct, int64_t ch, int64_t cw, int32_t pad_mode,
                     vsa_layout_t* out) {

@@ -114,7 +114,7 @@ struct KVCfg {
 
 struct KVSmall {
   uint64_t kv_full, final_bar;
-  uint64_t q_full[2], q_empty[2], s_full[2], s_free[2], pd_full[2], pd_empty[2];
+  uint64_t q_full[2], q_empty[2], s_full[2], s_free[2], pd_full[2], pd_empty[2], ds_done[2];
   uint32_t tmem;
 };
 
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                            const int32_t* __restrict__ idx, const float* __restrict__ dkc,
                            const float* __restrict__ dvc, int raster, __nv_bfloat16* __restrict__ dk,
                            __nv_bfloat16* __restrict__ dv, const __grid_constant__ CUtensorMap tm_ds,
-                           const int32_t* __restrict__ ds_pos, int ds_store) {
+                           const int32_t* __restrict__ ds_pos, int ds_store, TraceCfg tr) {
   using C = KVCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
@@ -157,8 +157,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&sm->q_full[b], 1);
       mbar_init(&sm->q_empty[b], 1);
       mbar_init(&sm->s_full[b], 1);
-      mbar_init(&sm->s_free[b], 128);
-      mbar_init(&sm->pd_full[b], 128);
+      mbar_init(&sm->s_free[b], kCompute);
+      mbar_init(&sm->pd_full[b], kCompute);
+      mbar_init(&sm->ds_done[b], 1);
       mbar_init(&sm->pd_empty[b], 1);
     }
     fence_barrier_init();
@@ -179,7 +180,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   tc_fence_after();
   const uint32_t tbase = sm->tmem;
 
-  if (warp == 8) {
+  if (warp == 9) {
+    // dS tile store: once all compute threads wrote pair p's dS (pd_full), TMA-store the
+    // bf16 [64 q][64 keys] tiles for the dQ GEMM — tile (qcube, t) at rows
+    // ((u*nc + qcube)*k + t)*64, t = position of kc in sel[qcube] — and release the buffer.
+    if (lane == 0 && ds_store) {
+      tma_prefetch_desc(&tm_ds);
+      const int64_t base = u * int64_t(L.nc) * k_sel;
+      for (int p = 0; p < npairs; ++p) {
+        const int b = p & 1;
+        mbar_wait(&sm->pd_full[b], (p >> 1) & 1);
+        const int e = beg + 2 * p;
+        uint8_t* myS = sS + b * 16384;
+        tma_store_2d(&tm_ds, myS, 0, int((base + int64_t(list[e]) * k_sel + ds_pos[base + e]) * 64));
+        if (2 * p + 1 < nq)
+          tma_store_2d(&tm_ds, myS + 8192, 0, int((base + int64_t(list[e + 1]) * k_sel + ds_pos[base + e + 1]) * 64));
+        bulk_commit_group();
+        bulk_wait_group_read0();
+        mbar_arrive(&sm->ds_done[b]);
+      }
+      bulk_wait_group0();
+    }
+  } else if (warp == 8) {
     if (lane == 0 && npairs > 0) {
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
@@ -195,7 +217,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int qa = list[beg + 2 * p];
         const bool hb = 2 * p + 1 < nq;
         const int qb = hb ? list[beg + 2 * p + 1] : 0;
+        trace_ev(tr, 1, p);
         mbar_wait(&sm->q_empty[st], ((p >> 1) & 1) ^ 1);
+        trace_ev(tr, 2, p);
         mbar_arrive_expect_tx(&sm->q_full[st], (hb ? 2 : 1) * 2 * C::kCube);
         uint8_t* q_dst = sQ + st * C::kPair;
         uint8_t* o_dst = sO + st * C::kPair;
@@ -234,9 +258,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                       make_sdesc_sw128(aV + offc, 16, 1024), idSD, s > 0);
           }
           umma_commit(&sm->s_full[st]);
+          trace_ev(tr, 3, ns);
           ++ns;
         }
         if (no < ns && mbar_test_wait(&sm->pd_full[no & 1], (no >> 1) & 1)) {
+          trace_ev(tr, 4, no);
           const int st = no & 1;
           tc_fence_after();
           const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
@@ -259,12 +285,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       umma_commit(&sm->final_bar);
     }
   } else if (warp < 8) {
-    const int g = warp >> 2;                 // warpgroup: pairs p = g (mod 2)
+    // All 8 compute warps work on every pair: warp w owns TMEM lanes 32*(w%4).. (query
+    // rows) and key columns [32*ch, 32*ch+32), ch = w/4 — half the per-pair latency of a
+    // whole-row split, which shortens how long each Q/dO stage is held.
+    const int g = warp >> 2;                 // column half
     const int ql = (warp & 3) * 32 + lane;   // query lane within the pair
     const uint32_t lrow = tbase + (uint32_t((warp & 3) * 32) << 16);
-    uint8_t* myP = sP + g * 16384;
-    uint8_t* myS = sS + g * 16384;
-    for (int p = g; p < npairs; p += 2) {
+    for (int p = 0; p < npairs; ++p) {
+      const int b = p & 1;
+      uint8_t* myP = sP + b * 16384;
+      uint8_t* myS = sS + b * 16384;
       const bool valid = ql < 64 || (2 * p + 1 < nq);  // warp-uniform
       float lse2 = 0.f, dl = 0.f;
       if (valid) {
@@ -273,60 +303,50 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         lse2 = lse[trow] * 1.4426950408889634f;
         dl = delta[trow];
       }
-      mbar_wait(&sm->s_full[g], (p >> 1) & 1);
+      if (threadIdx.x == 0) trace_ev(tr, 5, p);
+      mbar_wait(&sm->s_full[b], (p >> 1) & 1);
+      if (threadIdx.x == 0) trace_ev(tr, 6, p);
       tc_fence_after();
-      uint32_t pp[32], pd[32];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      uint32_t pp[16], pd[16];
+      {
         uint32_t rs[32], rd[32];
-        tmem_ld32_raw(lrow + g * 64 + h * 32, rs);
-        tmem_ld32_raw(lrow + 128 + g * 64 + h * 32, rd);
+        tmem_ld32_raw(lrow + b * 64 + g * 32, rs);
+        tmem_ld32_raw(lrow + 128 + b * 64 + g * 32, rd);
         tmem_wait_ld();
+        if (threadIdx.x == 0) trace_ev(tr, 8, p);
+        tc_fence_before();
+        mbar_arrive(&sm->s_free[b]);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const float p0 = ex2b(fmaf(__uint_as_float(rs[2 * j]), scale_log2, -lse2));
           const float p1 = ex2b(fmaf(__uint_as_float(rs[2 * j + 1]), scale_log2, -lse2));
-          pp[h * 16 + j] = pack_bf16(p0, p1);
-          pd[h * 16 + j] = pack_bf16(p0 * (__uint_as_float(rd[2 * j]) - dl), p1 * (__uint_as_float(rd[2 * j + 1]) - dl));
+          pp[j] = pack_bf16(p0, p1);
+          pd[j] = pack_bf16(p0 * (__uint_as_float(rd[2 * j]) - dl), p1 * (__uint_as_float(rd[2 * j + 1]) - dl));
         }
       }
-      tc_fence_before();
-      mbar_arrive(&sm->s_free[g]);
+      if (threadIdx.x == 0) trace_ev(tr, 9, p);
       if (!valid) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) pp[j] = pd[j] = 0u;
+        for (int j = 0; j < 16; ++j) pp[j] = pd[j] = 0u;
       }
       if (p >= 2) {
-        mbar_wait(&sm->pd_empty[g], ((p >> 1) - 1) & 1);
-        if (ds_store && ql == 0) bulk_wait_group_read0();  // previous dS tile store has read myS
-        named_bar_b(2 + g, 128);
+        mbar_wait(&sm->pd_empty[b], ((p >> 1) - 1) & 1);          // dV/dK MMAs of pair p-2 done
+        if (threadIdx.x == 0) trace_ev(tr, 10, p);
+        if (ds_store) mbar_wait(&sm->ds_done[b], ((p >> 1) - 1) & 1);  // its dS store has read myS
+        if (threadIdx.x == 0) trace_ev(tr, 11, p);
       }
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        *reinterpret_cast<uint4*>(myP + sw128_offset(ql, c * 16)) =
+      for (int c = 0; c < 4; ++c) {
+        *reinterpret_cast<uint4*>(myP + sw128_offset(ql, (g * 4 + c) * 16)) =
             make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]);
-        *reinterpret_cast<uint4*>(myS + sw128_offset(ql, c * 16)) =
+        *reinterpret_cast<uint4*>(myS + sw128_offset(ql, (g * 4 + c) * 16)) =
             make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
       }
       fence_proxy_async_smem();
-      if (ds_store) {
-        // materialise the bf16 dS tiles [64 q][64 keys] for the dQ GEMM: tile (qcube, t) at
-        // rows ((u*nc + qcube)*k + t)*64 of the dS store, t = position of kc in sel[qcube]
-        named_bar_b(2 + g, 128);
-        if (ql == 0) {
-          const int64_t base = u * int64_t(L.nc) * k_sel;
-          const int e = beg + 2 * p;
-          tma_store_2d(&tm_ds, myS, 0, int((base + int64_t(list[e]) * k_sel + ds_pos[base + e]) * 64));
-          if (2 * p + 1 < nq)
-            tma_store_2d(&tm_ds, myS + 8192, 0,
-                         int((base + int64_t(list[e + 1]) * k_sel + ds_pos[base + e + 1]) * 64));
-          bulk_commit_group();
-        }
-      }
       tc_fence_before();
-      mbar_arrive(&sm->pd_full[g]);
+      mbar_arrive(&sm->pd_full[b]);
+      if (threadIdx.x == 0) trace_ev(tr, 7, p);
     }
-    if (ds_store && ql == 0) bulk_wait_group0();
     // ---------------------------------------------------------------- epilogue
     float* stK = reinterpret_cast<float*>(sQ);                 // [64][D] fp32
     float* stV = reinterpret_cast<float*>(sQ + 64 * D * 4);    // [64][D] fp32
@@ -788,7 +808,8 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     kern<<<grid, kBwdThreads, smem, st>>>(tq, tk, tv, tdo, L, int(top_k), scale, scale_log2, lse, delta, offs, idx,
                                          dkc, dvc, raster, static_cast<__nv_bfloat16*>(dk),
-                                         static_cast<__nv_bfloat16*>(dv), tds, pos, store_ds ? 1 : 0);
+                                         static_cast<__nv_bfloat16*>(dv), tds, pos, store_ds ? 1 : 0,
+                                         debug_trace());
     int rc = kernel_status("fine_dkdv_sm100_kernel");
     if (rc) return rc;
   }

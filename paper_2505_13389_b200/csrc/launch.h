@@ -5,9 +5,13 @@
 
 #include <cuda_runtime.h>
 
+#include "sm100.cuh"
 #include "vsa_b200.h"
 
 namespace vsa_host {
+
+// debug event trace target (vsa_debug_trace); buf == nullptr when disabled
+vsa_dev::TraceCfg debug_trace();
 
 int launch_tile_pool(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, int32_t n, const void* const* xr,
                      void* const* xt, float* const* pooled, int32_t pool_mode, int in_tiled, cudaStream_t st);

@@ -34,6 +34,19 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// ---------------------------------------------------------------- debug event trace
+// One CTA (cta_x, cta_y) stores clock64 of event (code, index) into buf[code*256 + index]
+// (fire-and-forget stores, no atomics: non-perturbing). Disabled when buf == nullptr.
+struct TraceCfg {
+  unsigned long long* buf;
+  int cap, cta_x, cta_y;
+};
+__device__ __forceinline__ void trace_ev(const TraceCfg& t, int code, int idx) {
+  if (t.buf != nullptr && int(blockIdx.x) == t.cta_x && int(blockIdx.y) == t.cta_y && idx < 256 &&
+      code * 256 + idx < t.cap)
+    t.buf[code * 256 + idx] = clock64();
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -107,6 +120,10 @@ __device__ __forceinline__ void bulk_wait_group_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// ... all but the most recent committed group have finished reading shared memory.
+__device__ __forceinline__ void bulk_wait_group_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 
 // 1-D bulk copy global -> shared (no swizzle), completion via mbarrier tx-count.
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
