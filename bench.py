@@ -44,6 +44,9 @@ CONFIGS = {
     "dit": dict(workload="DiT pretraining batch", grid=(16, 32, 32), B=8, H=16, d=64, top_k=32),
     "wan14": dict(workload="Wan2.1-14B 720p layer (1 GPU, all heads)", grid=(21, 45, 80), B=1, H=40, d=128,
                   top_k=144),
+    # BASELINE configs[3]: sequence-parallel over the GPUs with the Ulysses all-to-all
+    "wan14sp": dict(workload="Wan2.1-14B 720p layer, Ulysses sequence-parallel", grid=(21, 45, 80), B=1, H=40,
+                    d=128, top_k=144, sp=True),
 }
 
 STAGES = ["tile_pool", "coarse_fwd", "fine_fwd", "prologue", "coarse_bwd", "fine_bwd"]
@@ -327,6 +330,125 @@ def run_ours(args, rank, world, local_rank):
     return line
 
 
+def run_sp(args, rank, world, local_rank):
+    """Ulysses sequence parallelism (BASELINE configs[3]): rank r holds the
+    sequence shard [B, S/P, H, d] of q, k, v, gates and dO; the all-to-alls reshard to
+    H/P heads x the whole sequence and back. Total work is fixed: strong scaling."""
+    import torch
+
+    import paper_2505_13389_b200 as vsa
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = CONFIGS[args.config]
+    dtype = torch.bfloat16
+    L = vsa.TileLayout(*cfg["grid"], pad=True)
+    nc, S, d, K, B, H = L.num_cubes, L.seq_len, cfg["d"], cfg["top_k"], cfg["B"], cfg["H"]
+    fl = flops(cfg, nc, K, d)
+    peaks = load_peaks()
+    u = vsa.UlyssesVsa(L, B, H, d, K, dtype=dtype)
+    P, Sc = u.x.P, u.x.Sc
+    g = torch.Generator(device=dev)
+    g.manual_seed(4321 + rank)
+    shards = [torch.randn((B, Sc, H, d), generator=g, device=dev, dtype=torch.float32).to(dtype) for _ in range(6)]
+
+    def step(xs):
+        out = u.forward(*xs[:5])
+        return (out,) + tuple(u.backward(xs[5]))
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step(shards)
+    barrier()
+    lib = vsa.lib()
+    n0 = lib.vsa_kernel_launches()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            step(shards)
+        e1.record(st)
+        barrier()
+    launches = lib.vsa_kernel_launches() - n0
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    value = fl["total"] / (ms * 1e-3) / 1e12
+
+    stage_ms = {s: 0.0 for s in STAGES}
+    nrep = max(2, min(args.steps, 3))
+    for _ in range(nrep):
+        u.op.trace = []
+        step(shards)
+        torch.cuda.synchronize()
+        tr = u.op.trace
+        for (_, a), (name, b) in zip(tr[:-1], tr[1:]):
+            if name in stage_ms:
+                stage_ms[name] += a.elapsed_time(b) / nrep
+    u.op.trace = None
+
+    # e2e: pinned host shards in, the six results out, every step
+    hin = [t.cpu().pin_memory() for t in shards]
+    hout = [torch.empty((B, Sc, H, d), dtype=dtype, pin_memory=True) for _ in range(6)]
+
+    def e2e_step():
+        xs = [h.to(dev, non_blocking=True) for h in hin]
+        for o, r in zip(hout, step(xs)):
+            o.copy_(r, non_blocking=True)
+
+    e2e_step()
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ne = max(1, min(args.steps, 3))
+    e2.record(st)
+    for _ in range(ne):
+        e2e_step()
+    e3.record(st)
+    barrier()
+    ems = max_over_ranks(e2.elapsed_time(e3) / ne)
+    if rank != 0:
+        return None
+    h2d = sum(t.numel() * t.element_size() for t in hin)
+    dom = max(("fine_fwd", "fine_bwd"), key=lambda s: stage_ms[s])
+    fl_rank = flops(dict(B=B, H=H // P), nc, K, d)  # per-rank share (each rank owns H/P heads)
+    ach = fl_rank[dom] / (stage_ms[dom] * 1e-3) / 1e12
+    stages = {s: {"ms": round(stage_ms[s], 4)} for s in STAGES}
+    for s in ("fine_fwd", "fine_bwd", "coarse_fwd", "coarse_bwd"):
+        if stage_ms[s] > 0:
+            stages[s]["tflops"] = round(fl_rank[s] / (stage_ms[s] * 1e-3) / 1e12, 1)
+    return {
+        "metric": "VSA fwd+bwd effective TFLOPS (algorithmic FLOPs / device time), Wan2.1-14B layer",
+        "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (torch.randn, seeded per rank)",
+        "config": {"workload": cfg["workload"], "B": B, "H": H, "head_dim": d, "grid": list(cfg["grid"]),
+                   "grid_padded": list(L.padded), "cube": [4, 4, 4], "num_cubes": nc, "top_k": K,
+                   "sparsity": round(1 - K / nc, 4), "global_batch": B, "seq_len": S,
+                   "parallelism": f"sp{P} (Ulysses all-to-all over NCCL, {H // P} heads per GPU)",
+                   "l2": "inputs larger than L2", "flops_per_step": fl["total"]},
+        "frac_of_peak": round(value / world / peaks["bf16_sust"], 4),
+        "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(ach, 1), "peak": peaks["bf16_sust"],
+                     "peak_kind": f"bf16_tflops_sustained ({peaks['src']})", "unit": "TFLOP/s",
+                     "frac": round(ach / peaks["bf16_sust"], 4), "traffic": None,
+                     "algorithmic_flops_per_launch": fl_rank[dom]},
+        "stages": stages,
+        "e2e": {"value": round(fl["total"] / (ems * 1e-3) / 1e12, 3), "unit": "TFLOP/s", "ms_per_step": round(ems, 3),
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+
 def cpu_baseline(cfg, reps):
     """The oracle (CPU restatement of the reference) on ONE (b,h) head of the
     workload: coarse fwd + fine fwd + fine bwd + coarse bwd, all host threads."""
@@ -414,7 +536,7 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        line = run_ours(args, rank, world, local_rank)
+        line = (run_sp if CONFIGS[args.config].get("sp") else run_ours)(args, rank, world, local_rank)
         if line is not None:
             print(json.dumps(line), flush=True)
     finally:

@@ -36,6 +36,12 @@ enum { VSA_F32 = 0, VSA_BF16 = 1 };
 enum { VSA_POOL_MEAN = 0, VSA_POOL_MAX = 1 };            /* PoolMode, coarse.hpp:13 */
 enum { VSA_PAD_REJECT = 0, VSA_PAD_ZERO = 1 };           /* layout.cpp:10-11 rejects; ZERO = extension */
 enum { VSA_GATE_IDENTITY = 0, VSA_GATE_SIGMOID = 1 };    /* GateActivation, vsa.hpp:9 */
+/* Raster I/O order of the raster-ordered tensors (q, k, v, gates, out, dO, grads).
+ * HEAD_MAJOR: [B, H, S, d] (AttnTensor, tensor.hpp:44-123).
+ * SEQ_MAJOR : [S/chunk][B][chunk][H][d]; chunk = S is the DiT-native [B, S, H, d]
+ *             (SURVEY.md §8f2), chunk = S/P is the receive buffer of a Ulysses
+ *             sequence->head all-to-all over P ranks, consumed in place (§8e). */
+enum { VSA_IO_HEAD_MAJOR = 0, VSA_IO_SEQ_MAJOR = 1 };
 
 /* Fine-stage epilogue flags (vsa_fine_forward). */
 enum {
@@ -56,7 +62,10 @@ typedef struct vsa_layout_t {
   int64_t seq_padded;     /* nc*cube */
   int64_t nc;             /* number of cubes */
   int32_t pad_mode;
-  int32_t reserved;
+  int32_t io_order;       /* raster I/O order, VSA_IO_* (vsa_layout_set_io); 0 after vsa_layout_make */
+  int64_t io_batch;       /* B (VSA_IO_SEQ_MAJOR only) */
+  int64_t io_heads;       /* H (VSA_IO_SEQ_MAJOR only) */
+  int64_t io_chunk;       /* sequence chunk, divides seq (VSA_IO_SEQ_MAJOR only) */
 } vsa_layout_t;
 
 /* Last error message of the calling thread ("" if none). */
@@ -75,6 +84,12 @@ int vsa_debug_trace(void* buf, int32_t cap, int32_t cta_x, int32_t cta_y);
  * extents up to cube multiples. */
 int vsa_layout_make(int64_t t, int64_t h, int64_t w, int64_t ct, int64_t ch, int64_t cw, int32_t pad_mode,
                     vsa_layout_t* out);
+
+/* Extension (no reference counterpart; the reference's AttnTensor is always
+ * [B,H,S,d]): select the raster I/O order for every call that takes this layout.
+ * SEQ_MAJOR needs batch, heads (bh = batch*heads at each call) and a chunk that
+ * divides t*h*w; HEAD_MAJOR ignores them. Tiled/cube tensors are unaffected. */
+int vsa_layout_set_io(vsa_layout_t* layout, int32_t order, int64_t batch, int64_t heads, int64_t chunk);
 
 /* Replaces: flatten_index (layout.cpp:40-42); host-side, no device work.
  * Out-of-range coordinates -> VSA_EINVAL (raster_index, layout.cpp:33-38). */
@@ -178,6 +193,13 @@ size_t vsa_fine_backward_workspace_bytes(const vsa_layout_t* layout, int64_t bh,
  * token of x (tiled) per (cube, channel) into dx (raster if `raster` else tiled, dtype). */
 int vsa_unpool_max_add(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled,
                        const float* dxc, int32_t raster, void* dx, void* stream);
+
+/* Ulysses resharding copy: dst[i1][i0] = src[i0][i1] over an
+ * [n0][n1] grid of contiguous blocks of `block_bytes` (a multiple of 16). With
+ * n0 = B*S/P, n1 = P, block = (H/P)*d*elem it packs a sequence shard [B,S/P,H,d]
+ * into the per-destination send buffer [P][B][S/P][H/P][d] (and, swapped, unpacks
+ * the returned head groups). 128-bit loads and stores, one pass. */
+int vsa_transpose_blocks(const void* src, void* dst, int64_t n0, int64_t n1, int64_t block_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -11,3 +11,4 @@ from .api import (  # noqa: F401
     coarse_forward_select, coarse_from_pooled, fine_backward, fine_forward, flatten_index, gate_backward,
     gates_from_hidden, pool_cubes, selection_transpose, tile, tile_pool, untile, validate_selection,
 )
+from .ulysses import UlyssesExchange, UlyssesVsa, transpose_blocks_cuda  # noqa: F401,E402

@@ -19,19 +19,22 @@ VSA_F32, VSA_BF16 = 0, 1
 POOL_MEAN, POOL_MAX = 0, 1
 PAD_REJECT, PAD_ZERO = 0, 1
 FINE_COMBINE, FINE_UNTILE, FINE_ADAPTATION, FINE_FORCE_SIMT = 1, 2, 4, 8
+IO_HEAD_MAJOR, IO_SEQ_MAJOR = 0, 1
 
 
 class vsa_layout_t(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("t", "h", "w", "ct", "ch", "cw", "tp", "hp", "wp", "nt", "nh", "nw",
-                                         "cube", "seq", "seq_padded", "nc")] + [("pad_mode", C.c_int32),
-                                                                                 ("reserved", C.c_int32)]
+                                         "cube", "seq", "seq_padded", "nc")] + [
+        ("pad_mode", C.c_int32), ("io_order", C.c_int32), ("io_batch", C.c_int64), ("io_heads", C.c_int64),
+        ("io_chunk", C.c_int64)]
 
 
 EXPORTS = [
     "vsa_last_error", "vsa_version", "vsa_kernel_launches", "vsa_debug_trace", "vsa_layout_make", "vsa_flatten_index", "vsa_tile", "vsa_untile",
     "vsa_tile_pool", "vsa_pool_tiled", "vsa_coarse_forward", "vsa_coarse_bitmap_bytes", "vsa_selection_transpose",
     "vsa_validate_selection", "vsa_fine_forward", "vsa_backward_prologue", "vsa_coarse_backward",
-    "vsa_fine_backward", "vsa_fine_backward_workspace_bytes", "vsa_unpool_max_add",
+    "vsa_fine_backward", "vsa_fine_backward_workspace_bytes", "vsa_unpool_max_add", "vsa_layout_set_io",
+    "vsa_transpose_blocks",
 ]
 
 
@@ -66,6 +69,8 @@ def lib():
     sig = {
         "vsa_layout_make": [I64] * 6 + [I32, LP],
         "vsa_debug_trace": [P, I32, I32, I32],
+        "vsa_layout_set_io": [LP, I32, I64, I64, I64],
+        "vsa_transpose_blocks": [P, P, I64, I64, I64, P],
         "vsa_flatten_index": [LP, I64, I64, I64, C.POINTER(I64)],
         "vsa_tile": [LP, I64, I64, I32, P, P, P],
         "vsa_untile": [LP, I64, I64, I32, P, P, P],

@@ -332,13 +332,22 @@ class VsaOp:
     fine epilogue) or tile-ordered (``raster=False``, the reference's vsa_forward
     contract, vsa.hpp:86). Buffers are allocated once (HBM-resident artifacts,
     the VsaOutput of vsa.hpp:56-63).
+
+    ``io="bshd"`` (raster only) reads and writes the raster tensors sequence-major
+    instead: [B, S, H, d] (DiT-native), or with ``seq_chunks=P`` the
+    Ulysses receive layout [P, B, S/P, H, d] (§8e) — consumed in place, no copies.
     """
 
     def __init__(self, layout: TileLayout, B: int, H: int, d: int, top_k: int, dtype=torch.bfloat16,
                  pool: int = POOL_MEAN, adaptation: bool = False, raster: bool = True, device="cuda",
-                 force_simt: bool = False, bwd_workspace: bool = True):
+                 force_simt: bool = False, bwd_workspace: bool = True, io: str = "bhsd", seq_chunks: int = 1):
         if not (1 <= top_k <= layout.num_cubes):
             raise ValueError("coarse_forward_select: k must be in [1, num_cubes]")
+        if io not in ("bhsd", "bshd"):
+            raise ValueError("io must be 'bhsd' or 'bshd'")
+        if io == "bshd" and not raster:
+            raise ValueError("sequence-major I/O needs raster=True")
+        self.io, self.seq_chunks = io, int(seq_chunks)
         self.layout, self.B, self.H, self.d, self.top_k = layout, B, H, d, int(top_k)
         self.dtype, self.pool, self.adaptation, self.raster = dtype, pool, adaptation, raster
         self.force_simt = force_simt
@@ -368,6 +377,17 @@ class VsaOp:
         self._gc = self._gf = None
         self._lib = L.lib()
         self._lref = layout.ref()
+        S = layout.seq_len
+        if io == "bshd":
+            if self.seq_chunks < 1 or S % self.seq_chunks:
+                raise ValueError("seq_chunks must divide the raster sequence length")
+            self._raw = L.vsa_layout_t.from_buffer_copy(layout._raw)
+            check(self._lib.vsa_layout_set_io(C.byref(self._raw), L.IO_SEQ_MAJOR, B, H, S // self.seq_chunks))
+            self._lref = C.byref(self._raw)
+            self.io_shape = ((B, S, H, d) if self.seq_chunks == 1 else
+                             (self.seq_chunks, B, S // self.seq_chunks, H, d))
+        else:
+            self.io_shape = (B, H, S if raster else layout.seq_padded, d)
         self.trace = None  # optional list: (stage, torch.cuda.Event) appended after each stage
 
     def _mark(self, name):
@@ -381,12 +401,22 @@ class VsaOp:
         return self.layout.seq_len if self.raster else self.layout.seq_padded
 
     def _chk(self, t, name):
-        _cuda4(t, name)
-        if tuple(t.shape) != (self.B, self.H, self.seq_io, self.d) or t.dtype != self.dtype:
-            raise ValueError(f"{name}: expected {(self.B, self.H, self.seq_io, self.d)} {self.dtype}")
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise ValueError(f"{name}: expected a CUDA tensor")
+        shp = tuple(t.shape)
+        if self.io == "bshd" and len(shp) == 5 and shp[0] == 1:
+            shp = shp[1:]  # [1, B, S, H, d]: the chunked layout with one chunk
+        if shp != self.io_shape or t.dtype != self.dtype:
+            raise ValueError(f"{name}: expected {self.io_shape} {self.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: must be contiguous")
 
-    def forward(self, q, k, v, gc, gf=None, out=None, sel_override=None, check_inputs=True):
-        """vsa_forward (vsa.hpp:89-122) at attention level: gates are given."""
+    def forward(self, q, k, v, gc, gf=None, out=None, sel_override=None, check_inputs=True, before_fine=None):
+        """vsa_forward (vsa.hpp:89-122) at attention level: gates are given.
+
+        ``before_fine``: optional callable run after the coarse stage, before the
+        fine kernel (the first reader of the gates) — e.g. to wait for a gate
+        exchange that overlapped K1-K3."""
         lib, lr, st = self._lib, self._lref, _stream()
         B, H, d = self.B, self.H, self.d
         bh = B * H
@@ -430,7 +460,9 @@ class VsaOp:
         else:
             self.fine_sel, self.fine_k = self.sel, self.top_k
         if out is None:
-            out = torch.empty((B, self.H, self.seq_io, d), dtype=self.dtype, device=q.device)
+            out = torch.empty(self.io_shape, dtype=self.dtype, device=q.device)
+        if before_fine is not None:
+            before_fine()
         flags = L.FINE_COMBINE | (L.FINE_UNTILE if self.raster else 0) | (L.FINE_ADAPTATION if self.adaptation else 0)
         if self.force_simt:
             flags |= L.FINE_FORCE_SIMT
@@ -451,7 +483,7 @@ class VsaOp:
         B, H, d = self.B, self.H, self.d
         bh = B * H
         dt = L.VSA_BF16 if self.dtype == torch.bfloat16 else L.VSA_F32
-        mk = lambda: torch.empty((B, H, self.seq_io, d), dtype=self.dtype, device=dout.device)
+        mk = lambda: torch.empty(self.io_shape, dtype=self.dtype, device=dout.device)
         dq = mk() if dq is None else dq
         dk = mk() if dk is None else dk
         dv = mk() if dv is None else dv

@@ -46,6 +46,15 @@ static int vec_elems(int32_t dt) { return dt == VSA_BF16 ? 8 : 4; }
 static int check_layout(const vsa_layout_t* L) {
   VSA_REQUIRE(L != nullptr, "layout: null pointer");
   VSA_REQUIRE(L->nc >= 1 && L->cube >= 1 && L->seq_padded == L->nc * L->cube, "layout: not initialised");
+  VSA_REQUIRE(L->io_order == VSA_IO_HEAD_MAJOR || L->io_order == VSA_IO_SEQ_MAJOR, "layout: unknown io order");
+  return 0;
+}
+
+// Sequence-major raster I/O addresses rows by (b, h) = (u / H, u % H): the unit
+// count must be the layout's B*H.
+static int check_io(const vsa_layout_t* L, int64_t bh) {
+  if (L->io_order == VSA_IO_SEQ_MAJOR)
+    VSA_REQUIRE(bh == L->io_batch * L->io_heads, "sequence-major I/O: bh must equal batch*heads of the layout");
   return 0;
 }
 
@@ -105,6 +114,23 @@ int vsa_layout_make(int64_t t, int64_t h, int64_t w, int64_t ct, int64_t ch, int
   return VSA_OK;
 }
 
+int vsa_layout_set_io(vsa_layout_t* L, int32_t order, int64_t batch, int64_t heads, int64_t chunk) {
+  VSA_CHECKED(check_layout(L));
+  VSA_REQUIRE(order == VSA_IO_HEAD_MAJOR || order == VSA_IO_SEQ_MAJOR, "layout_set_io: unknown order");
+  if (order == VSA_IO_HEAD_MAJOR) {
+    L->io_order = order;
+    L->io_batch = L->io_heads = L->io_chunk = 0;
+    return VSA_OK;
+  }
+  VSA_REQUIRE(batch >= 1 && heads >= 1, "layout_set_io: batch and heads must be >= 1");
+  VSA_REQUIRE(chunk >= 1 && L->seq % chunk == 0, "layout_set_io: chunk must divide the raster sequence length");
+  L->io_order = order;
+  L->io_batch = batch;
+  L->io_heads = heads;
+  L->io_chunk = chunk;
+  return VSA_OK;
+}
+
 int vsa_flatten_index(const vsa_layout_t* L, int64_t t, int64_t h, int64_t w, int64_t* out) {
   VSA_CHECKED(check_layout(L));
   VSA_REQUIRE(t >= 0 && t < L->t && h >= 0 && h < L->h && w >= 0 && w < L->w,
@@ -118,6 +144,7 @@ int vsa_flatten_index(const vsa_layout_t* L, int64_t t, int64_t h, int64_t w, in
 int vsa_tile(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* x_raster, void* x_tiled,
              void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(dtype_ok(dtype), "tile: unknown dtype");
   VSA_CHECKED(check_vec_dim(d, dtype));
   VSA_REQUIRE(bh >= 1 && x_raster && x_tiled, "tile: bad arguments");
@@ -129,6 +156,7 @@ int vsa_tile(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const 
 int vsa_untile(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled, void* x_raster,
                void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(dtype_ok(dtype), "untile: unknown dtype");
   VSA_CHECKED(check_vec_dim(d, dtype));
   VSA_REQUIRE(bh >= 1 && x_raster && x_tiled, "untile: bad arguments");
@@ -139,6 +167,7 @@ int vsa_tile_pool(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, i
                   const void* const* x_raster, void* const* x_tiled, float* const* pooled, int32_t pool_mode,
                   void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(dtype_ok(dtype), "tile_pool: unknown dtype");
   VSA_CHECKED(check_vec_dim(d, dtype));
   VSA_REQUIRE(n >= 1 && n <= 3 && x_raster && bh >= 1, "tile_pool: 1..3 tensors");
@@ -150,6 +179,7 @@ int vsa_tile_pool(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, i
 int vsa_pool_tiled(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled, float* pooled,
                    int32_t pool_mode, void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(dtype_ok(dtype), "pool_cubes: unknown dtype");
   VSA_CHECKED(check_vec_dim(d, dtype));
   VSA_REQUIRE(pool_mode == VSA_POOL_MEAN || pool_mode == VSA_POOL_MAX, "pool_cubes: unknown pool mode");
@@ -168,6 +198,7 @@ int vsa_coarse_forward(const vsa_layout_t* L, int64_t bh, int64_t d, const float
                        const float* vc, int64_t top_k, float* ac, float* oc_cube, int32_t* sel, int32_t* selT_offs,
                        int32_t* selT_idx, void* bitmap_ws, void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(top_k >= 1 && top_k <= L->nc, "coarse_forward_select: k must be in [1, num_cubes]");
   VSA_REQUIRE(d >= 1 && d <= 1024, "coarse_forward_select: head_dim out of range");
   VSA_REQUIRE(qc && kc && vc && ac && oc_cube && sel && bh >= 1, "coarse_forward_select: null buffer");
@@ -181,6 +212,7 @@ int vsa_coarse_forward(const vsa_layout_t* L, int64_t bh, int64_t d, const float
 int vsa_selection_transpose(const vsa_layout_t* L, int64_t bh, const int32_t* sel, int64_t top_k,
                             int32_t* selT_offs, int32_t* selT_idx, void* bitmap_ws, void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(top_k >= 1 && top_k <= L->nc, "BlockSelection: k must be in [1, num_cubes]");
   VSA_REQUIRE(sel && selT_offs && selT_idx && bitmap_ws && bh >= 1, "selection_transpose: null buffer");
   return launch_selection_transpose(*L, bh, sel, top_k, selT_offs, selT_idx, bitmap_ws, as_stream(stream));
@@ -197,6 +229,7 @@ int vsa_fine_forward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype
                      const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse, float* row_max,
                      const void* gc, const void* gf, const float* oc_cube, int32_t flags, void* out, void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(dtype_ok(dtype), "fine stage: unknown dtype");
   VSA_REQUIRE(q && k && v && sel && o_fine && lse && bh >= 1, "fine stage: null buffer");
   VSA_REQUIRE(top_k >= 1 && top_k <= L->nc, "fine stage: selection does not match shapes");
@@ -217,6 +250,7 @@ int vsa_backward_prologue(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t 
                           int32_t adaptation, void* dof, float* delta, float* doc_cube, void* dgc, void* dgf,
                           void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(dtype_ok(dtype), "vsa_backward: unknown dtype");
   VSA_CHECKED(check_vec_dim(d, dtype));
   VSA_REQUIRE(dout && gc && oc_cube && o_fine && dof && delta && bh >= 1,
@@ -230,6 +264,7 @@ int vsa_coarse_backward(const vsa_layout_t* L, int64_t bh, int64_t d, const floa
                         const float* vc, const float* ac, const float* doc_cube, float* dqc, float* dkc, float* dvc,
                         float* scratch, void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(ac != nullptr, "coarse_backward: artifacts do not match layout");
   VSA_REQUIRE(qc && kc && vc && doc_cube && dqc && dkc && dvc && scratch && bh >= 1 && d >= 1 && d <= 1024,
               "coarse_backward: null buffer");
@@ -242,6 +277,7 @@ int vsa_fine_backward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtyp
                       const float* dkc, const float* dvc, int32_t raster, int32_t flags, void* dq, void* dk,
                       void* dv, void* workspace, size_t workspace_bytes, void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(dtype_ok(dtype), "fine_backward: unknown dtype");
   VSA_REQUIRE(q && k && v && dof && sel && dq && dk && dv && bh >= 1, "fine_backward: null buffer");
   VSA_REQUIRE(lse && delta, "fine_backward: saved statistics do not match shapes");
@@ -264,6 +300,7 @@ size_t vsa_fine_backward_workspace_bytes(const vsa_layout_t* L, int64_t bh, int6
 int vsa_unpool_max_add(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled,
                        const float* dxc, int32_t raster, void* dx, void* stream) {
   VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(dtype_ok(dtype), "unpool: unknown dtype");
   VSA_REQUIRE(x_tiled && dxc && dx && bh >= 1 && d >= 1 && d <= 1024, "unpool: null buffer");
   return launch_unpool_max_add(*L, bh, d, dtype, x_tiled, dxc, raster, dx, as_stream(stream));

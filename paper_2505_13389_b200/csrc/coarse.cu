@@ -259,7 +259,7 @@ __global__ void unpool_max_kernel(DevLayout L, int d, const T* __restrict__ x, c
   if (raster) {
     const int64_t r = raster_of_tile(L, int64_t(c) * L.cube + am);
     if (r < 0) return;
-    row = u * L.seq + r;
+    row = raster_row(L, u, r);
   } else {
     row = base + am;
   }

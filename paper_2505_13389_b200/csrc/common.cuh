@@ -21,6 +21,9 @@ struct DevLayout {
   int nc;          // number of cubes
   int64_t seq;     // t*h*w
   int64_t seqp;    // nc*cube
+  // raster I/O order (vsa_layout_set_io): 0 = [B,H,S,d]; 1 = [S/chunk][B][chunk][H][d]
+  int io;
+  int64_t io_batch, io_heads, io_chunk;
 };
 
 inline DevLayout to_dev(const vsa_layout_t& L) {
@@ -30,7 +33,21 @@ inline DevLayout to_dev(const vsa_layout_t& L) {
   d.nt = int(L.nt); d.nh = int(L.nh); d.nw = int(L.nw);
   d.cube = int(L.cube); d.nc = int(L.nc);
   d.seq = L.seq; d.seqp = L.seq_padded;
+  d.io = int(L.io_order);
+  d.io_batch = L.io_batch; d.io_heads = L.io_heads; d.io_chunk = L.io_chunk;
   return d;
+}
+
+// Row (token vector) index of raster token r of unit u = b*H + h in a raster-order
+// I/O tensor. Head-major [B,H,S,d]: u*S + r. Sequence-major (io = 1):
+// [S/chunk][B][chunk][H][d] — with chunk = S the DiT-native [B,S,H,d]; with
+// chunk = S/P the receive buffer of a Ulysses all-to-all over P ranks (rank j's
+// sequence shard is chunk j), consumed in place.
+__host__ __device__ __forceinline__ int64_t raster_row(const DevLayout& L, int64_t u, int64_t r) {
+  if (L.io == 0) return u * L.seq + r;
+  const int64_t b = u / L.io_heads, h = u - b * L.io_heads;
+  const int64_t j = r / L.io_chunk, s = r - j * L.io_chunk;
+  return ((j * L.io_batch + b) * L.io_chunk + s) * L.io_heads + h;
 }
 
 // Raster position of tile position `pos` (cube rank * cube + offset); -1 for a pad token.

@@ -88,7 +88,7 @@ __device__ __forceinline__ void write_rows(const DevLayout& L, int64_t u, int cu
     if (raster) {
       const int64_t rr = raster_of_tile(L, int64_t(cube) * 64 + r);
       if (rr < 0) continue;
-      row = u * L.seq + rr;
+      row = raster_row(L, u, rr);
     }
     store16(dst + row * D + ch * 8, v);
   }

@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         if (untile) {
           const int64_t r = raster_of_tile(L, int64_t(qc) * 64 + q);
           if (r < 0) continue;
-          row = u * L.seq + r;
+          row = raster_row(L, u, r);
         }
         if (combine) {
           float g1[8], g2[8];

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kSimtThreads) fine_fwd_simt_kernel(
         if (untile) {
           const int64_t rr = raster_of_tile(L, int64_t(qc) * B + i);
           if (rr < 0) continue;
-          row = u * L.seq + rr;
+          row = raster_row(L, u, rr);
         }
         float val = o;
         if (combine) {
@@ -139,7 +139,7 @@ __device__ __forceinline__ void store_grad(const DevLayout& L, int64_t u, int cu
   if (raster) {
     const int64_t rr = raster_of_tile(L, int64_t(cube_idx) * L.cube + i);
     if (rr < 0) return;
-    row = u * L.seq + rr;
+    row = raster_row(L, u, rr);
   }
   dx[row * d + c] = from_f<T>(val);
 }

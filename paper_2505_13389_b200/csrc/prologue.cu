@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(128) prologue_kernel(DevLayout L, int64_t bh, 
     if (raster && active) {
       const int64_t r = raster_of_tile(L, pos);
       valid = r >= 0;
-      srow = u * L.seq + r;
+      srow = raster_row(L, u, r);
     }
     float part = 0.f;
     if (valid) {

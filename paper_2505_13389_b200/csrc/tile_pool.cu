@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
         float v[V];
         const bool valid = in_tiled || (t < L.t && h < L.h && w < L.w);
         if (valid) {
-          const int64_t row = in_tiled ? tile_base + o : u * L.seq + (int64_t(t) * L.h + h) * L.w + w;
+          const int64_t row = in_tiled ? tile_base + o : raster_row(L, u, (int64_t(t) * L.h + h) * L.w + w);
           load16(x + row * d + ch * V, v);
         } else {
 #pragma unroll
@@ -98,7 +98,7 @@ __global__ void untile_kernel(DevLayout L, int64_t bh, int d, const T* __restric
     const int64_t u = rowt / L.seqp, pos = rowt - u * L.seqp;
     const int64_t r = raster_of_tile(L, pos);
     if (r < 0) continue;
-    *reinterpret_cast<uint4*>(x + (u * L.seq + r) * d + ch * V) =
+    *reinterpret_cast<uint4*>(x + raster_row(L, u, r) * d + ch * V) =
         *reinterpret_cast<const uint4*>(xt + rowt * d + ch * V);
   }
 }
