@@ -36,6 +36,7 @@
 namespace vsa_dev {
 
 constexpr int kBwdThreads = 352;
+constexpr int kKVThreads = 384;  // dK/dV: + a load-watcher warp
 constexpr int kCompute = 256;  // two warpgroups
 
 __device__ __forceinline__ float ex2b(float x) {
@@ -43,7 +44,20 @@ __device__ __forceinline__ float ex2b(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ void named_bar_b(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+__device__ __forceinline__ void named_bar_b(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// Hardware named barriers between the dK/dV roles. The MMA issuer never polls an
+// mbarrier: mbarrier waits are shared-memory reads, which the SS MMA operand
+// stream starves (profiles/smem_contention_r1.txt: ~13 B/cycle left for threads),
+// so each poll costs ~150-250 cycles of issue time. Producer->issuer signals use
+// bar.arrive (compute warps) / bar.sync (issuer); TMA completions are turned into
+// named-barrier rendezvous by a watcher warp. Each ID carries one event kind in
+// strict order (a producer cannot arrive twice before the issuer syncs: see the
+// p_empty / ds_empty waits), sd_free alternates by pair parity, granules rotate
+// over 4 IDs with bar.sync on both sides.
+constexpr int kBarPFull = 2, kBarDsFull = 3, kBarSdFree = 4 /* 4,5 */, kBarGran = 6 /* 6..9 */;
 
 __device__ __forceinline__ void tmem_ld32_raw(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -65,6 +79,37 @@ __device__ __forceinline__ void stage_cols(uint32_t taddr_lane, int c0, float* s
   tmem_ld32(taddr_lane + c0, t);
 #pragma unroll
   for (int i = 0; i < 32; ++i) st[(c0 + i) * D + dl] = t[i] * scale;
+}
+
+// Output row (token vector) index of row r of cube `cube` of unit u: raster (or -1 for a
+// pad token) or tiled. Computed once per CTA (off the epilogue's critical path).
+__device__ __forceinline__ int64_t cube_out_row(const DevLayout& L, int64_t u, int cube, int r, int raster) {
+  if (!raster) return u * L.seqp + int64_t(cube) * 64 + r;
+  const int64_t rr = raster_of_tile(L, int64_t(cube) * 64 + r);
+  return rr < 0 ? -1 : raster_row(L, u, rr);
+}
+
+// As write_rows, with the cube-level unpool term already in a D-float row (smem) and
+// the 64 output row indices precomputed (rows[r] < 0: pad token, dropped).
+template <int D>
+__device__ __forceinline__ void write_rows_x(const DevLayout& L, int64_t u, int cube, const float* st,
+                                             const float* xrow, const int64_t* rows, __nv_bfloat16* __restrict__ dst,
+                                             int tid, int nthr) {
+  constexpr int CH = D / 8;
+  const float inv = 1.0f / float(L.cube);
+  for (int task = tid; task < 64 * CH; task += nthr) {
+    const int r = task / CH, ch = task - r * CH;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = st ? st[r * D + ch * 8 + i] : 0.f;
+    if (xrow) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] += xrow[ch * 8 + i] * inv;
+    }
+    const int64_t row = rows[r];
+    if (row < 0) continue;
+    store16(dst + row * D + ch * 8, v);
+  }
 }
 
 // Write a [64][D] fp32 staged tile as bf16 rows of cube `cube`, adding xc/64 (mean unpool).
@@ -95,31 +140,65 @@ __device__ __forceinline__ void write_rows(const DevLayout& L, int64_t u, int cu
 }
 
 // ============================================================================ dK / dV
+// KV-stationary, one CTA per key cube. The streamed operands live in a ring of
+// NG "granules", each holding ONE pair of cubes of ONE tensor: item 2p = Q(p),
+// item 2p+1 = dO(p) go to granule i % NG. Q and dO are released separately — dO(p)
+// when dV(p) completes, Q(p) when dK(p) does — and P / dS have their own buffers,
+// so a pair's operands are held only as long as each product needs them. The
+// products of pair p are four in-order tensor streams:
+//   S(p)  = Qpair . K^T   -> s_full    (needs Q(p))
+//   dP(p) = dOpair . V^T  -> dp_full   (needs dO(p))
+//   dV(p) += dOpair^T . P -> frees dO(p), P buffer   (needs P(p) from the compute warps)
+//   dK(p) += Qpair^T . dS -> frees Q(p),  dS buffer  (needs dS(p))
+// The compute warps write P(p) as soon as S(p) is in, before dP(p) is read, so
+// dV(p) overlaps the dS math.
+// Granule of streamed item i (item 2p = Q(p), 2p+1 = dO(p)). Granules are handed
+// out in the order they are released: the first NG items take granules 0..NG-1,
+// then item NG+j takes the granule of the j-th release. The tensor pipe releases
+// dO(p) (after dV(p)) before Q(p) (after dK(p)), so the j-th release is item j^1.
+// Must be called for i = 0, 1, 2, ... in order; keeps 16 x 4-bit history.
+template <int NG>
+struct GranSeq {
+  uint64_t hist = 0;
+  __device__ __forceinline__ int next(int i) {
+    const int g = (i < NG) ? i : int((hist >> ((((i - NG) ^ 1) & 15) * 4)) & 15u);
+    const int sh = (i & 15) * 4;
+    hist = (hist & ~(uint64_t(15) << sh)) | (uint64_t(g) << sh);
+    return g;
+  }
+};
+
 template <int D>
 struct KVCfg {
   static constexpr int kChunks = D / 64;
   static constexpr int kCube = 64 * D * 2;      // one cube
-  static constexpr int kPair = 128 * D * 2;     // one pair of cubes
+  static constexpr int kGran = 128 * D * 2;     // one pair of cubes of one tensor
+  static constexpr int kNPB = 1;                // P / dS buffers
+  static constexpr int kNG = D == 128 ? 5 : 10;  // granules
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + kCube;
-  static constexpr int kOffQ = kOffV + kCube;           // 2 stages
-  static constexpr int kOffO = kOffQ + 2 * kPair;       // 2 stages
-  static constexpr int kOffP = kOffO + 2 * kPair;       // 2 x (128 x 128 B)
-  static constexpr int kOffS = kOffP + 2 * 16384;       // 2 x (128 x 128 B)
-  static constexpr int kOffZ = kOffS + 2 * 16384;
+  static constexpr int kOffG = kOffV + kCube;
+  static constexpr int kOffP = kOffG + kNG * kGran;     // kNPB x (128 x 128 B)
+  static constexpr int kOffS = kOffP + kNPB * 16384;    // kNPB x (128 x 128 B)
+  static constexpr int kOffZ = kOffS + kNPB * 16384;
   static constexpr int kTiles = kOffZ + (D == 64 ? 16384 : 0);
   static constexpr int kPairChunk = 16384;  // 128 rows x 128 B
   static constexpr int kCubeChunk = 8192;   // 64 rows x 128 B
+  static_assert(kTiles <= 225 * 1024, "dK/dV smem budget");
 };
 
 struct KVSmall {
+  alignas(16) float xk[128], xv[128];  // cube-level unpool rows dKc, dVc of this key cube
+  int64_t rows[64];                      // output row of each token of the key cube
   uint64_t kv_full, final_bar;
-  uint64_t q_full[2], q_empty[2], s_full[2], s_free[2], pd_full[2], pd_empty[2], ds_done[2];
+  uint64_t g_full[10], g_empty[10];
+  uint64_t s_full[2], dp_full[2], sd_free[2];
+  uint64_t p_full[2], p_empty[2], ds_full[2], ds_empty[2], ds_stored[2];
   uint32_t tmem;
 };
 
 template <int D>
-__global__ void __launch_bounds__(kBwdThreads, 1)
+__global__ void __launch_bounds__(kKVThreads, 1)
     fine_dkdv_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                            DevLayout L, int k_sel, float scale, float scale_log2, const float* __restrict__ lse,
@@ -129,17 +208,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                            __nv_bfloat16* __restrict__ dv, const __grid_constant__ CUtensorMap tm_ds,
                            const int32_t* __restrict__ ds_pos, int ds_store, TraceCfg tr) {
   using C = KVCfg<D>;
+  constexpr int NG = C::kNG, NPB = C::kNPB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sK = smem + C::kOffK;
   uint8_t* sV = smem + C::kOffV;
-  uint8_t* sQ = smem + C::kOffQ;
-  uint8_t* sO = smem + C::kOffO;
+  uint8_t* sG = smem + C::kOffG;
   uint8_t* sP = smem + C::kOffP;
   uint8_t* sS = smem + C::kOffS;
   uint8_t* sZ = smem + C::kOffZ;
   KVSmall* sm = reinterpret_cast<KVSmall*>(smem + C::kTiles);
 
+  if (threadIdx.x == 0) trace_ev(tr, 24, 0);
   const int warp = int(warp_id()), lane = int(lane_id());
   const int kc = blockIdx.x;
   const int64_t u = blockIdx.y;
@@ -151,26 +231,34 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 10) tmem_alloc<512>(&sm->tmem);
   if (threadIdx.x == 0) {
+    trace_ev(tr, 24, 4);
     mbar_init(&sm->kv_full, 1);
     mbar_init(&sm->final_bar, 1);
+    for (int g = 0; g < NG; ++g) {
+      mbar_init(&sm->g_full[g], 1);
+      mbar_init(&sm->g_empty[g], 1);
+    }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm->q_full[b], 1);
-      mbar_init(&sm->q_empty[b], 1);
       mbar_init(&sm->s_full[b], 1);
-      mbar_init(&sm->s_free[b], kCompute);
-      mbar_init(&sm->pd_full[b], kCompute);
-      mbar_init(&sm->ds_done[b], 1);
-      mbar_init(&sm->pd_empty[b], 1);
+      mbar_init(&sm->dp_full[b], 1);
+      mbar_init(&sm->sd_free[b], kCompute);
+    }
+    for (int b = 0; b < NPB; ++b) {
+      mbar_init(&sm->p_full[b], kCompute);
+      mbar_init(&sm->p_empty[b], 1);
+      mbar_init(&sm->ds_full[b], kCompute);
+      mbar_init(&sm->ds_empty[b], 1);
+      mbar_init(&sm->ds_stored[b], 1);
     }
     fence_barrier_init();
   }
-  // zero the second half of both Q/dO stages (a single-cube last pair must see finite data)
-  if (nq & 1) {
-    for (int i = threadIdx.x; i < 4 * C::kChunks * 512; i += blockDim.x) {
-      const int t = i / (C::kChunks * 512), rem = i - t * C::kChunks * 512;
-      uint8_t* base = (t < 2 ? sQ : sO) + (t & 1) * C::kPair;
-      reinterpret_cast<uint4*>(base + (rem / 512) * C::kPairChunk + 8192)[rem % 512] = make_uint4(0, 0, 0, 0);
-    }
+  // a single-cube last pair reads rows 64..127 of its granules: make them finite once
+  // (later occupants leave loaded bf16 data behind); their P / dS rows are forced to 0
+  if ((nq & 1) && 2 * (npairs - 1) < NG) {
+    // items 2(npairs-1), 2(npairs-1)+1 take fresh granules 2(npairs-1).. (GranSeq: i < NG -> i)
+    const int g0 = 2 * (npairs - 1), ng = min(2, NG - g0);
+    for (int i = threadIdx.x; i < ng * C::kGran / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(sG + g0 * C::kGran)[i] = make_uint4(0, 0, 0, 0);
   }
   if (D == 64)
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) reinterpret_cast<uint4*>(sZ)[i] = make_uint4(0, 0, 0, 0);
@@ -180,16 +268,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   tc_fence_after();
   const uint32_t tbase = sm->tmem;
 
-  if (warp == 9) {
-    // dS tile store: once all compute threads wrote pair p's dS (pd_full), TMA-store the
-    // bf16 [64 q][64 keys] tiles for the dQ GEMM — tile (qcube, t) at rows
-    // ((u*nc + qcube)*k + t)*64, t = position of kc in sel[qcube] — and release the buffer.
-    if (lane == 0 && ds_store) {
+  if (warp == 9 && lane == 1 && tr.buf != nullptr && int(blockIdx.x) == tr.cta_x && int(blockIdx.y) == tr.cta_y) {
+    // debug watcher: completion times of the four product groups of every pair
+    for (int p = 0; p < npairs; ++p) {  // only S completions: never lags behind
+      mbar_wait(&sm->s_full[p & 1], (p >> 1) & 1);
+      trace_ev(tr, 16, p);
+    }
+  } else if (warp == 9) {
+    // dS tile store: TMA-store the bf16 [64 q][64 keys] tiles of pair p for the dQ GEMM
+    // — tile (qcube, t) at rows ((u*nc + qcube)*k + t)*64, t = position of kc in
+    // sel[qcube] — then release the buffer to the compute warps.
+    if (lane == 0 && ds_store && !(tr.ablate & 2)) {
       tma_prefetch_desc(&tm_ds);
       const int64_t base = u * int64_t(L.nc) * k_sel;
       for (int p = 0; p < npairs; ++p) {
-        const int b = p & 1;
-        mbar_wait(&sm->pd_full[b], (p >> 1) & 1);
+        const int b = p % NPB;
+        mbar_wait(&sm->ds_full[b], (p / NPB) & 1);
         const int e = beg + 2 * p;
         uint8_t* myS = sS + b * 16384;
         tma_store_2d(&tm_ds, myS, 0, int((base + int64_t(list[e]) * k_sel + ds_pos[base + e]) * 64));
@@ -197,7 +291,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tma_store_2d(&tm_ds, myS + 8192, 0, int((base + int64_t(list[e + 1]) * k_sel + ds_pos[base + e + 1]) * 64));
         bulk_commit_group();
         bulk_wait_group_read0();
-        mbar_arrive(&sm->ds_done[b]);
+        mbar_arrive(&sm->ds_stored[b]);
       }
       bulk_wait_group0();
     }
@@ -212,89 +306,144 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_load_2d(sK + c * C::kCubeChunk, &tm_k, &sm->kv_full, c * 64, row0 + kc * 64);
         tma_load_2d(sV + c * C::kCubeChunk, &tm_v, &sm->kv_full, c * 64, row0 + kc * 64);
       }
-      for (int p = 0; p < npairs; ++p) {
-        const int st = p & 1;
+      GranSeq<NG> seq;
+      uint32_t fills = 0;  // bit g: parity of the fills of granule g so far
+      for (int i = 0; i < 2 * npairs; ++i) {
+        const int p = i >> 1, g = seq.next(i);
+        const CUtensorMap* tm = (i & 1) ? &tm_do : &tm_q;
         const int qa = list[beg + 2 * p];
         const bool hb = 2 * p + 1 < nq;
         const int qb = hb ? list[beg + 2 * p + 1] : 0;
-        trace_ev(tr, 1, p);
-        mbar_wait(&sm->q_empty[st], ((p >> 1) & 1) ^ 1);
-        trace_ev(tr, 2, p);
-        mbar_arrive_expect_tx(&sm->q_full[st], (hb ? 2 : 1) * 2 * C::kCube);
-        uint8_t* q_dst = sQ + st * C::kPair;
-        uint8_t* o_dst = sO + st * C::kPair;
+        if ((tr.ablate & 4) && i >= NG) break;  // debug: stream no further loads
+        mbar_wait(&sm->g_empty[g], ((fills >> g) & 1) ^ 1);
+        fills ^= 1u << g;
+        trace_ev(tr, 2, i);
+        mbar_arrive_expect_tx(&sm->g_full[g], (hb ? 2 : 1) * C::kCube);
+        uint8_t* dst = sG + g * C::kGran;
         for (int c = 0; c < C::kChunks; ++c) {
-          tma_load_2d(q_dst + c * C::kPairChunk, &tm_q, &sm->q_full[st], c * 64, row0 + qa * 64);
-          tma_load_2d(o_dst + c * C::kPairChunk, &tm_do, &sm->q_full[st], c * 64, row0 + qa * 64);
-          if (hb) {
-            tma_load_2d(q_dst + c * C::kPairChunk + 8192, &tm_q, &sm->q_full[st], c * 64, row0 + qb * 64);
-            tma_load_2d(o_dst + c * C::kPairChunk + 8192, &tm_do, &sm->q_full[st], c * 64, row0 + qb * 64);
-          }
+          tma_load_2d(dst + c * C::kPairChunk, tm, &sm->g_full[g], c * 64, row0 + qa * 64);
+          if (hb) tma_load_2d(dst + c * C::kPairChunk + 8192, tm, &sm->g_full[g], c * 64, row0 + qb * 64);
         }
+      }
+    }
+  } else if (warp == 11) {
+    // load watcher: waits for each streamed granule's TMA, then meets the issuer at a
+    // named barrier (it runs at most one item ahead per barrier ID)
+    if (npairs > 0 && !(tr.ablate & 16)) {
+      GranSeq<NG> seq;
+      uint32_t fills = 0;
+      for (int i = 0; i < 2 * npairs; ++i) {
+        const int g = seq.next(i);
+        if (!(tr.ablate & 4) || i < NG) mbar_wait_warp(&sm->g_full[g], (fills >> g) & 1);
+        fills ^= 1u << g;
+        named_bar_b(kBarGran + (i & 3), 64);
       }
     }
   } else if (warp == 10) {
-    if (lane == 0 && npairs > 0) {
-      const uint32_t idSD = make_idesc_bf16(128, 64, false, false);
-      const uint32_t idG = make_idesc_bf16(128, 64, true, true);
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aO = smem_u32(sO);
-      const uint32_t aP = smem_u32(sP), aS = smem_u32(sS);
-      mbar_wait(&sm->kv_full, 0);
-      // Event-driven issue of two in-order streams: {S, dP}(ns) and {dV, dK}(no).
-      int ns = 0, no = 0;
-      while (no < npairs) {
-        if (ns < npairs && mbar_test_wait(&sm->q_full[ns & 1], (ns >> 1) & 1) &&
-            (ns < 2 || mbar_test_wait(&sm->s_free[ns & 1], ((ns >> 1) - 1) & 1))) {
-          const int st = ns & 1;
-          tc_fence_after();
-          const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
-#pragma unroll
-          for (int s = 0; s < D / 16; ++s) {
-            const uint32_t off = (s >> 2) * C::kPairChunk + (s & 3) * 32;
-            const uint32_t offc = (s >> 2) * C::kCubeChunk + (s & 3) * 32;
-            umma_bf16(tbase + st * 64, make_sdesc_sw128(q0 + off, 16, 1024), make_sdesc_sw128(aK + offc, 16, 1024),
-                      idSD, s > 0);
-            umma_bf16(tbase + 128 + st * 64, make_sdesc_sw128(o0 + off, 16, 1024),
-                      make_sdesc_sw128(aV + offc, 16, 1024), idSD, s > 0);
-          }
-          umma_commit(&sm->s_full[st]);
-          trace_ev(tr, 3, ns);
-          ++ns;
+    if (npairs > 0) {  // whole warp: warp-uniform issue, one elected lane issues
+      constexpr uint32_t idSD = make_idesc_bf16(128, 64, false, false);
+      constexpr uint32_t idG = make_idesc_bf16(128, 64, true, true);
+      const uint32_t aG = smem_u32(sG), aP = smem_u32(sP), aS = smem_u32(sS);
+      // descriptor bases; K-steps advance the start address (+32 B = +2 encoded)
+      const uint64_t dK0 = make_sdesc_sw128(smem_u32(sK), 16, 1024), dV0 = make_sdesc_sw128(smem_u32(sV), 16, 1024);
+      const uint64_t dG0 = make_sdesc_sw128(aG, 16, 1024);
+      GranSeq<NG> seq;
+      int gq[2], go[2];  // granules of Q / dO of the pairs in flight (by pair parity)
+      mbar_wait_warp(&sm->kv_full, 0);
+      // S(n) = Qpair.K^T and dP(n) = dOpair.V^T into TMEM buffer n&1
+      auto issue_s = [&](int n) {
+        const int b = n & 1;
+        const int g0 = seq.next(2 * n);
+        gq[b] = g0;
+        if (!(tr.ablate & 16)) {
+          if (n >= 2) named_bar_b(kBarSdFree + b, kCompute + 32);
+          named_bar_b(kBarGran + ((2 * n) & 3), 64);
         }
-        if (no < ns && mbar_test_wait(&sm->pd_full[no & 1], (no >> 1) & 1)) {
-          trace_ev(tr, 4, no);
-          const int st = no & 1;
-          tc_fence_after();
-          const uint32_t q0 = aQ + st * C::kPair, o0 = aO + st * C::kPair;
-          const uint32_t p0 = aP + st * 16384, s0 = aS + st * 16384;
-          const uint32_t lbo_q = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - q0;
-          const uint32_t lbo_o = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - o0;
+        tc_fence_after();
+        if (lane == 0) trace_ev(tr, 14, n);
+        const uint64_t q0 = dG0 + uint64_t((g0 * C::kGran) >> 4);
 #pragma unroll
-          for (int s = 0; s < 8; ++s) {
-            const uint32_t acc = (no > 0 || s > 0) ? 1u : 0u;
-            umma_bf16(tbase + 256, make_sdesc_sw128(o0 + s * 2048, lbo_o, 1024),
-                      make_sdesc_sw128(p0 + s * 2048, 8192, 1024), idG, acc);
-            umma_bf16(tbase + 320, make_sdesc_sw128(q0 + s * 2048, lbo_q, 1024),
-                      make_sdesc_sw128(s0 + s * 2048, 8192, 1024), idG, acc);
-          }
-          umma_commit(&sm->q_empty[st]);
-          umma_commit(&sm->pd_empty[st]);
-          ++no;
+        for (int s = 0; s < D / 16; ++s) {
+          umma_bf16_warp(tbase + b * 64, q0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
+                         dK0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
         }
+        umma_commit_warp(&sm->s_full[b]);
+        if (lane == 0) trace_ev(tr, 3, n);
+      };
+      auto issue_dp = [&](int n) {
+        const int b = n & 1;
+        const int g1 = seq.next(2 * n + 1);
+        go[b] = g1;
+        if (!(tr.ablate & 16)) named_bar_b(kBarGran + ((2 * n + 1) & 3), 64);
+        tc_fence_after();
+        if (lane == 0) trace_ev(tr, 15, n);
+        const uint64_t o0 = dG0 + uint64_t((g1 * C::kGran) >> 4);
+#pragma unroll
+        for (int s = 0; s < D / 16; ++s)
+          umma_bf16_warp(tbase + 128 + b * 64, o0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
+                         dV0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+        umma_commit_warp(&sm->dp_full[b]);
+        if (lane == 0) trace_ev(tr, 13, n);
+      };
+      // Fixed software-pipelined order per pair p:  S(p+1), dV(p), dP(p+1), dK(p).
+      // The exp / dS math of a pair runs a full period ahead of its dV / dK, and the
+      // granule of dO(p) is released (after dV(p)) early enough to refill dO(p+2)
+      // with NG = 5 (a load takes ~1200 cycles, a product group ~400).
+      issue_s(0);
+      issue_dp(0);
+      for (int p = 0; p < npairs; ++p) {
+        const int b = p & 1, pb = p % NPB;
+        if (p + 1 < npairs) issue_s(p + 1);
+        if (!(tr.ablate & 16)) named_bar_b(kBarPFull, kCompute + 32);
+        tc_fence_after();
+        if (lane == 0) trace_ev(tr, 1, p);
+        {
+          const uint32_t o0 = aG + go[b] * C::kGran;
+          const uint32_t lbo = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - o0;
+          const uint64_t da = make_sdesc_sw128(o0, lbo, 1024), db = make_sdesc_sw128(aP + pb * 16384, 8192, 1024);
+#pragma unroll
+          for (int s = 0; s < 8; ++s)
+            umma_bf16_warp(tbase + 256, da + uint64_t(s * 128), db + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+        }
+        umma_commit_warp(&sm->g_empty[go[b]]);
+        umma_commit_warp(&sm->p_empty[pb]);
+        if (lane == 0) trace_ev(tr, 4, p);
+        if (p + 1 < npairs) issue_dp(p + 1);
+        if (!(tr.ablate & 16)) named_bar_b(kBarDsFull, kCompute + 32);
+        tc_fence_after();
+        if (lane == 0) trace_ev(tr, 0, p);
+        {
+          const uint32_t q0 = aG + gq[b] * C::kGran;
+          const uint32_t lbo = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - q0;
+          const uint64_t da = make_sdesc_sw128(q0, lbo, 1024), db = make_sdesc_sw128(aS + pb * 16384, 8192, 1024);
+#pragma unroll
+          for (int s = 0; s < 8; ++s)
+            umma_bf16_warp(tbase + 320, da + uint64_t(s * 128), db + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+        }
+        umma_commit_warp(&sm->g_empty[gq[b]]);
+        umma_commit_warp(&sm->ds_empty[pb]);
+        if (lane == 0) trace_ev(tr, 12, p);
       }
-      umma_commit(&sm->final_bar);
+      umma_commit_warp(&sm->final_bar);
     }
   } else if (warp < 8) {
-    // All 8 compute warps work on every pair: warp w owns TMEM lanes 32*(w%4).. (query
-    // rows) and key columns [32*ch, 32*ch+32), ch = w/4 — half the per-pair latency of a
-    // whole-row split, which shortens how long each Q/dO stage is held.
-    const int g = warp >> 2;                 // column half
-    const int ql = (warp & 3) * 32 + lane;   // query lane within the pair
+    // 8 compute warps on every pair: warp w owns TMEM lanes 32*(w%4).. (query rows)
+    // and key columns [32*ch, 32*ch+32), ch = w/4.
+    const int ch = warp >> 2;
+    const int ql = (warp & 3) * 32 + lane;  // query lane within the pair
     const uint32_t lrow = tbase + (uint32_t((warp & 3) * 32) << 16);
-    for (int p = 0; p < npairs; ++p) {
-      const int b = p & 1;
-      uint8_t* myP = sP + b * 16384;
-      uint8_t* myS = sS + b * 16384;
+    // prefetch the unpool rows now: the epilogue then has no dependent global loads
+    if (threadIdx.x < D) {
+      const int64_t o = (u * L.nc + kc) * D + threadIdx.x;
+      sm->xk[threadIdx.x] = dkc ? dkc[o] : 0.f;
+      sm->xv[threadIdx.x] = dvc ? dvc[o] : 0.f;
+    } else if (threadIdx.x < D + 64) {
+      sm->rows[threadIdx.x - D] = cube_out_row(L, u, kc, threadIdx.x - D, raster);
+    }
+    for (int p = 0; p < ((tr.ablate & 16) ? 0 : npairs); ++p) {
+      const int b = p & 1, pb = p % NPB, use = p / NPB;
+      uint8_t* myP = sP + pb * 16384;
+      uint8_t* myS = sS + pb * 16384;
       const bool valid = ql < 64 || (2 * p + 1 < nq);  // warp-uniform
       float lse2 = 0.f, dl = 0.f;
       if (valid) {
@@ -303,67 +452,88 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         lse2 = lse[trow] * 1.4426950408889634f;
         dl = delta[trow];
       }
+      mbar_wait_sleep(&sm->s_full[b], (p >> 1) & 1);
       if (threadIdx.x == 0) trace_ev(tr, 5, p);
-      mbar_wait(&sm->s_full[b], (p >> 1) & 1);
-      if (threadIdx.x == 0) trace_ev(tr, 6, p);
       tc_fence_after();
-      uint32_t pp[16], pd[16];
-      {
-        uint32_t rs[32], rd[32];
-        tmem_ld32_raw(lrow + b * 64 + g * 32, rs);
-        tmem_ld32_raw(lrow + 128 + b * 64 + g * 32, rd);
+      float pf[32];
+      uint32_t pk[16];
+      if (tr.ablate & 1) {  // debug: no TMEM load, no exp
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pf[j] = lse2 * 1e-30f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = 0u;
+      } else {
+        uint32_t rs[32];
+        tmem_ld32_raw(lrow + b * 64 + ch * 32, rs);
         tmem_wait_ld();
-        if (threadIdx.x == 0) trace_ev(tr, 8, p);
-        tc_fence_before();
-        mbar_arrive(&sm->s_free[b]);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float p0 = ex2b(fmaf(__uint_as_float(rs[2 * j]), scale_log2, -lse2));
-          const float p1 = ex2b(fmaf(__uint_as_float(rs[2 * j + 1]), scale_log2, -lse2));
-          pp[j] = pack_bf16(p0, p1);
-          pd[j] = pack_bf16(p0 * (__uint_as_float(rd[2 * j]) - dl), p1 * (__uint_as_float(rd[2 * j + 1]) - dl));
-        }
-      }
-      if (threadIdx.x == 0) trace_ev(tr, 9, p);
-      if (!valid) {
+        for (int j = 0; j < 32; ++j) pf[j] = valid ? ex2b(fmaf(__uint_as_float(rs[j]), scale_log2, -lse2)) : 0.f;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) pp[j] = pd[j] = 0u;
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(pf[2 * j], pf[2 * j + 1]);
       }
-      if (p >= 2) {
-        mbar_wait(&sm->pd_empty[b], ((p >> 1) - 1) & 1);          // dV/dK MMAs of pair p-2 done
-        if (threadIdx.x == 0) trace_ev(tr, 10, p);
-        if (ds_store) mbar_wait(&sm->ds_done[b], ((p >> 1) - 1) & 1);  // its dS store has read myS
-        if (threadIdx.x == 0) trace_ev(tr, 11, p);
-      }
+      if (threadIdx.x == 0) trace_ev(tr, 6, p);
+      if (p >= NPB) mbar_wait_sleep(&sm->p_empty[pb], (use - 1) & 1);  // dV of the previous user done
+      if (threadIdx.x == 0) trace_ev(tr, 8, p);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        *reinterpret_cast<uint4*>(myP + sw128_offset(ql, (g * 4 + c) * 16)) =
-            make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]);
-        *reinterpret_cast<uint4*>(myS + sw128_offset(ql, (g * 4 + c) * 16)) =
-            make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
-      }
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(myP + sw128_offset(ql, (ch * 4 + c) * 16)) =
+            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&sm->pd_full[b]);
+      named_bar_arrive(kBarPFull, kCompute + 32);
+      mbar_wait_sleep(&sm->dp_full[b], (p >> 1) & 1);
+      if (threadIdx.x == 0) trace_ev(tr, 9, p);
+      tc_fence_after();
+      if (tr.ablate & 1) {
+        tc_fence_before();
+        named_bar_arrive(kBarSdFree + b, kCompute + 32);
+      } else {
+        uint32_t rd[32];
+        tmem_ld32_raw(lrow + 128 + b * 64 + ch * 32, rd);
+        tmem_wait_ld();
+        tc_fence_before();
+        named_bar_arrive(kBarSdFree + b, kCompute + 32);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          pk[j] = pack_bf16(pf[2 * j] * (__uint_as_float(rd[2 * j]) - dl),
+                            pf[2 * j + 1] * (__uint_as_float(rd[2 * j + 1]) - dl));
+      }
+      if (threadIdx.x == 0) trace_ev(tr, 10, p);
+      if (p >= NPB) {
+        mbar_wait_sleep(&sm->ds_empty[pb], (use - 1) & 1);                 // dK of the previous user done
+        if (ds_store && !(tr.ablate & 2)) mbar_wait_sleep(&sm->ds_stored[pb], (use - 1) & 1);  // and its dS store read it
+      }
+      if (threadIdx.x == 0) trace_ev(tr, 11, p);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(myS + sw128_offset(ql, (ch * 4 + c) * 16)) =
+            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      fence_proxy_async_smem();
+      named_bar_arrive(kBarDsFull, kCompute + 32);
+      mbar_arrive(&sm->ds_full[pb]);  // for the dS store warp
       if (threadIdx.x == 0) trace_ev(tr, 7, p);
     }
     // ---------------------------------------------------------------- epilogue
-    float* stK = reinterpret_cast<float*>(sQ);                 // [64][D] fp32
-    float* stV = reinterpret_cast<float*>(sQ + 64 * D * 4);    // [64][D] fp32
+    float* stK = reinterpret_cast<float*>(sG);                 // [64][D] fp32
+    float* stV = reinterpret_cast<float*>(sG + 64 * D * 4);    // [64][D] fp32
     if (npairs > 0) {
-      mbar_wait(&sm->final_bar, 0);
+      mbar_wait_sleep(&sm->final_bar, 0);
+      if (threadIdx.x == 0) trace_ev(tr, 24, 1);
       tc_fence_after();
-      if (ql < D) {  // warpgroup 0 stages dK^T, warpgroup 1 dV^T
-        stage_cols<D>(lrow + (g ? 256 : 320), 0, g ? stV : stK, ql, g ? 1.f : scale);
-        stage_cols<D>(lrow + (g ? 256 : 320), 32, g ? stV : stK, ql, g ? 1.f : scale);
+      if (ql < D) {  // warps 0-3 stage dK^T, warps 4-7 dV^T
+        stage_cols<D>(lrow + (ch ? 256 : 320), 0, ch ? stV : stK, ql, ch ? 1.f : scale);
+        stage_cols<D>(lrow + (ch ? 256 : 320), 32, ch ? stV : stK, ql, ch ? 1.f : scale);
       }
     }
     named_bar_b(1, kCompute);
-    write_rows<D>(L, u, kc, npairs > 0 ? stK : nullptr, dkc, raster, dk, threadIdx.x, kCompute);
-    write_rows<D>(L, u, kc, npairs > 0 ? stV : nullptr, dvc, raster, dv, threadIdx.x, kCompute);
+    write_rows_x<D>(L, u, kc, npairs > 0 ? stK : nullptr, dkc ? sm->xk : nullptr, sm->rows, dk, threadIdx.x,
+                    kCompute);
+    write_rows_x<D>(L, u, kc, npairs > 0 ? stV : nullptr, dvc ? sm->xv : nullptr, sm->rows, dv, threadIdx.x,
+                    kCompute);
+    if (threadIdx.x == 0) trace_ev(tr, 24, 2);
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_ev(tr, 24, 3);
   if (warp == 10) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
@@ -806,7 +976,7 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
     const size_t smem = KVCfg<D>::kTiles + sizeof(KVSmall) + 1024;
     auto kern = fine_dkdv_sm100_kernel<D>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    kern<<<grid, kBwdThreads, smem, st>>>(tq, tk, tv, tdo, L, int(top_k), scale, scale_log2, lse, delta, offs, idx,
+    kern<<<grid, kKVThreads, smem, st>>>(tq, tk, tv, tdo, L, int(top_k), scale, scale_log2, lse, delta, offs, idx,
                                          dkc, dvc, raster, static_cast<__nv_bfloat16*>(dk),
                                          static_cast<__nv_bfloat16*>(dv), tds, pos, store_ds ? 1 : 0,
                                          debug_trace());

@@ -40,6 +40,7 @@ __device__ __forceinline__ bool elect_one() {
 struct TraceCfg {
   unsigned long long* buf;
   int cap, cta_x, cta_y;
+  int ablate;  // debug-only timing ablations (VSA_ABLATE env), 0 in normal runs
 };
 __device__ __forceinline__ void trace_ev(const TraceCfg& t, int code, int idx) {
   if (t.buf != nullptr && int(blockIdx.x) == t.cta_x && int(blockIdx.y) == t.cta_y && idx < 256 &&
@@ -89,9 +90,38 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the warp sleeps until the phase completes (or
+// the hint expires) instead of re-issuing the probe. Busy-polling warps steal issue
+// slots from the MMA-issuing warp of their SMSP (measured: the dK/dV issuer slowed
+// from 48 to 85-390 cycles per MMA with 2 polling warps on its SMSP).
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x100000u)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_sleep(bar, parity)) {
+  }
+}
+
+// Warp-uniform probe: lane 0's view, broadcast (all lanes must call it).
+__device__ __forceinline__ bool mbar_test_wait_warp(uint64_t* bar, uint32_t parity) {
+  return __shfl_sync(0xffffffffu, mbar_test_wait(bar, parity) ? 1 : 0, 0) != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
+}
+// Whole-warp wait that leaves the warp converged (lane 0 polls).
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  if ((threadIdx.x & 31u) == 0) mbar_wait(bar, parity);
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------- TMA
@@ -161,6 +191,29 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t adesc, uint6
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-collective variants: the WHOLE warp executes them (converged, warp-uniform
+// operands) and one lane, elected inside the asm, issues. Keeping the issue loop
+// warp-wide lets ptxas hold descriptors in uniform registers with no per-MMA
+// divergence handling; issuing from a single-lane branch costs ~2x the SS MMA time
+// per instruction (profiles/mma_issue_bench2_r1.txt vs mma_bench_r1.txt).
+__device__ __forceinline__ void umma_bf16_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // Arrive on an mbarrier when all previously issued tcgen05 ops of this thread complete.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))

@@ -71,7 +71,7 @@ __device__ __forceinline__ void mma4_elect(uint32_t d, uint64_t a, uint32_t at, 
   }
 }
 
-template <int N, bool kTS, int kStyle>
+template <int N, bool kTS, int kStyle, bool kMN = false>
 __global__ void __launch_bounds__(128, 1) bench(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* smem = align_smem_1024(raw);
@@ -90,15 +90,19 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, unsigned long long* o
   tc_fence_after();
   const uint32_t tbase = slot;
   if (threadIdx.x < 32) {
-    constexpr uint32_t idesc = make_idesc_bf16(128, N, false, false);
+    constexpr uint32_t idesc = make_idesc_bf16(128, N, kMN, kMN);
     const uint32_t a = smem_u32(smem), b = smem_u32(smem + 16384);
-    const uint64_t ad = make_sdesc_sw128(a, 16, 1024), bd = make_sdesc_sw128(b, 16, 1024);
+    // MN-major (as the fine kernels' transposed products): A = [2 x 64 M][K rows of 128 B],
+    // M blocks at LBO; B = N=64 [K rows of 128 B]; a K-step of 16 is +2048 B (+128 encoded)
+    const uint64_t ad = kMN ? make_sdesc_sw128(a, 8192, 1024) : make_sdesc_sw128(a, 16, 1024);
+    const uint64_t bd = kMN ? make_sdesc_sw128(b, 8192, 1024) : make_sdesc_sw128(b, 16, 1024);
+    constexpr uint64_t kstep = kMN ? 128 : 2;
     const uint32_t at = tbase + 256;
     const unsigned long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
       if constexpr (kStyle == 0) {
 #pragma unroll
-        for (int s = 0; s < 4; ++s) mma1_elect<kTS>(tbase, ad + 2 * s, at + 8 * s, bd + 2 * s, idesc);
+        for (int s = 0; s < 4; ++s) mma1_elect<kTS>(tbase, ad + kstep * s, at + 8 * s, bd + kstep * s, idesc);
       } else if constexpr (kStyle == 1) {
         mma4_elect<kTS>(tbase, ad, at, bd, idesc);
       } else {
@@ -128,10 +132,10 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, unsigned long long* o
   if (threadIdx.x < 32) tmem_dealloc<512>(tbase);
 }
 
-template <int N, bool kTS, int kStyle>
+template <int N, bool kTS, int kStyle, bool kMN = false>
 static int run(int nsm, unsigned long long* d) {
   const int smem = 16384 + 32768 + 1024;
-  auto k = bench<N, kTS, kStyle>;
+  auto k = bench<N, kTS, kStyle, kMN>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 4000;
   k<<<nsm, 128, smem>>>(50, d);
@@ -148,8 +152,8 @@ static int run(int nsm, unsigned long long* d) {
   const double per = avg / (iters * 4.0);
   const double ideal = 128.0 * N / 256.0;
   const double bytes = (kTS ? 0 : 128 * 32) + N * 32;
-  printf("style %d %s N=%3d: %6.1f cycles/MMA (floor %5.1f) -> %5.1f%% of peak, smem operands %6.1f B/cycle\n",
-         kStyle, kTS ? "TS" : "SS", N, per, ideal, 100.0 * ideal / per, bytes / per);
+  printf("style %d %s%s N=%3d: %6.1f cycles/MMA (floor %5.1f) -> %5.1f%% of peak, smem operands %6.1f B/cycle\n",
+         kStyle, kTS ? "TS" : "SS", kMN ? " MN-major" : "", N, per, ideal, 100.0 * ideal / per, bytes / per);
   return 0;
 }
 
@@ -160,6 +164,8 @@ int main() {
   cudaMalloc(&d, nsm * 8);
   int rc = 0;
   rc |= run<64, false, 0>(nsm, d);
+  rc |= run<64, false, 0, true>(nsm, d);
+  rc |= run<128, false, 0, true>(nsm, d);
   rc |= run<64, false, 1>(nsm, d);
   rc |= run<64, false, 2>(nsm, d);
   rc |= run<128, false, 0>(nsm, d);

@@ -11,9 +11,9 @@ import torch
 sys.path.insert(0, ".")
 import paper_2505_13389_b200 as vsa  # noqa: E402
 
-NAMES = {1: "prod_wait_empty", 2: "prod_issue", 3: "mma_SdP", 4: "mma_dVdK", 5: "cmp_wait_S", 6: "cmp_got_S",
-         7: "cmp_done", 8: "cmp_tmem_ld_done", 9: "cmp_math_done", 10: "cmp_pd_empty_ok", 11: "cmp_bulk_read_ok",
-         12: "cmp_bar_ok"}
+NAMES = {2: "prod_issue(item)", 3: "mma_S", 13: "mma_dP", 4: "mma_dV", 12: "mma_dK", 5: "cmp_got_S",
+         6: "cmp_P_ready", 8: "cmp_P_buf_free", 9: "cmp_got_dP", 10: "cmp_dS_ready", 11: "cmp_dS_buf_free",
+         7: "cmp_done"}
 
 L = vsa.TileLayout(21, 30, 52, pad=True)
 op = vsa.VsaOp(L, 1, 12, 128, 78)
@@ -23,7 +23,7 @@ for _ in range(2):
     op.forward(*x[:5])
     op.backward(x[5])
 torch.cuda.synchronize()
-cap = 16 * 256
+cap = 28 * 256
 buf = torch.zeros(cap, dtype=torch.int64, device="cuda")
 for cta in (300, 301):
     buf.zero_()
@@ -33,8 +33,23 @@ for cta in (300, 301):
     torch.cuda.synchronize()
     vsa.lib().vsa_debug_trace(None, 0, 0, 0)
     b = buf.cpu().tolist()
-    ev = sorted((b[i], i // 256, i % 256) for i in range(cap) if b[i] != 0)
-    t0 = ev[0][0]
-    print(f"=== dkdv cta {cta}: {len(ev)} events")
-    for c, code, idx in ev:
-        print(f"{c - t0:8d} {NAMES.get(code, code):18s} {idx}")
+    ev = {(i // 256, i % 256): b[i] for i in range(cap) if b[i] != 0}
+    t0 = ev.get((24, 0), min(ev.values()))
+    cols = [("ldQ", 2, lambda p: 2 * p), ("ldO", 2, lambda p: 2 * p + 1), ("S0", 14, None), ("S", 3, None),
+            ("dP0", 15, None), ("dP", 13, None), ("dV0", 1, None), ("dK0", 0, None),
+            ("gotS", 5, None), ("Prdy", 6, None), ("Pbuf", 8, None), ("gotdP", 9, None), ("dSrdy", 10, None),
+            ("dSbuf", 11, None), ("done", 7, None), ("dV", 4, None), ("dK", 12, None), ("xS", 16, None),
+            ("xdP", 17, None), ("xdV", 18, None), ("xdK", 19, None)]
+    print(f"=== dkdv cta {cta}: {len(ev)} events (cycles from first event; ld = TMA issue, S/dP/dV/dK = MMA issued)")
+    print("  p " + "".join(f"{n:>8s}" for n, _, _ in cols))
+    names = {0: "entry", 4: "after TMEM alloc", 1: "epilogue start", 2: "epilogue rows written", 3: "exit"}
+    print("  CTA:", {names[i]: ev[(24, i)] - t0 for i in names if (24, i) in ev}, "npairs ~", max(p for (c, p) in ev if c == 3) + 1)
+    for p in range(2, 10):
+        a, b, c = ev.get((14, p)), ev.get((3, p)), ev.get((16, p))
+        if None not in (a, b, c):
+            print(f"S({p}): issue {b - a} cycles, complete {c - a} cycles after issue start")
+    for p in range(64):
+        row = [ev.get((code, f(p) if f else p)) for _, code, f in cols]
+        if all(r is None for r in row):
+            break
+        print(f"{p:3d} " + "".join(f"{(r - t0) if r else -1:8d}" for r in row))
