@@ -55,9 +55,9 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
 // bar.arrive (compute warps) / bar.sync (issuer); TMA completions are turned into
 // named-barrier rendezvous by a watcher warp. Each ID carries one event kind in
 // strict order (a producer cannot arrive twice before the issuer syncs: see the
-// p_empty / ds_empty waits), sd_free alternates by pair parity, granules rotate
-// over 4 IDs with bar.sync on both sides.
-constexpr int kBarPFull = 2, kBarDsFull = 3, kBarSdFree = 4 /* 4,5 */, kBarGran = 6 /* 6..9 */;
+// p_empty / ds_empty waits), sd_free alternates by pair parity, and the granule
+// rendezvous is a bar.sync on both sides (pairs up in order on one ID).
+constexpr int kBarPFull = 2, kBarDsFull = 3, kBarSdFree = 4 /* 4,5 */, kBarGran = 6;
 
 __device__ __forceinline__ void tmem_ld32_raw(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -173,7 +173,7 @@ struct KVCfg {
   static constexpr int kChunks = D / 64;
   static constexpr int kCube = 64 * D * 2;      // one cube
   static constexpr int kGran = 128 * D * 2;     // one pair of cubes of one tensor
-  static constexpr int kNPB = 1;                // P / dS buffers
+  static constexpr int kNPB = 1;                // P / dS buffers (the issuer assumes 1)
   static constexpr int kNG = D == 128 ? 5 : 10;  // granules
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + kCube;
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     // dS tile store: TMA-store the bf16 [64 q][64 keys] tiles of pair p for the dQ GEMM
     // — tile (qcube, t) at rows ((u*nc + qcube)*k + t)*64, t = position of kc in
     // sel[qcube] — then release the buffer to the compute warps.
-    if (lane == 0 && ds_store && !(tr.ablate & 2)) {
+    if (lane == 0 && ds_store) {
       tma_prefetch_desc(&tm_ds);
       const int64_t base = u * int64_t(L.nc) * k_sel;
       for (int p = 0; p < npairs; ++p) {
@@ -314,7 +314,6 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int qa = list[beg + 2 * p];
         const bool hb = 2 * p + 1 < nq;
         const int qb = hb ? list[beg + 2 * p + 1] : 0;
-        if ((tr.ablate & 4) && i >= NG) break;  // debug: stream no further loads
         mbar_wait(&sm->g_empty[g], ((fills >> g) & 1) ^ 1);
         fills ^= 1u << g;
         trace_ev(tr, 2, i);
@@ -329,62 +328,61 @@ __global__ void __launch_bounds__(kKVThreads, 1)
   } else if (warp == 11) {
     // load watcher: waits for each streamed granule's TMA, then meets the issuer at a
     // named barrier (it runs at most one item ahead per barrier ID)
-    if (npairs > 0 && !(tr.ablate & 16)) {
+    if (npairs > 0) {
       GranSeq<NG> seq;
       uint32_t fills = 0;
       for (int i = 0; i < 2 * npairs; ++i) {
         const int g = seq.next(i);
-        if (!(tr.ablate & 4) || i < NG) mbar_wait_warp(&sm->g_full[g], (fills >> g) & 1);
+        mbar_wait_warp(&sm->g_full[g], (fills >> g) & 1);
         fills ^= 1u << g;
-        named_bar_b(kBarGran + (i & 3), 64);
+        named_bar_b(kBarGran, 64);  // rendezvous with the issuer, in consumption order
       }
     }
   } else if (warp == 10) {
     if (npairs > 0) {  // whole warp: warp-uniform issue, one elected lane issues
       constexpr uint32_t idSD = make_idesc_bf16(128, 64, false, false);
       constexpr uint32_t idG = make_idesc_bf16(128, 64, true, true);
-      const uint32_t aG = smem_u32(sG), aP = smem_u32(sP), aS = smem_u32(sS);
+      const uint32_t aG = smem_u32(sG), aP = smem_u32(sP), aS = smem_u32(sS);  // NPB = 1 (static_assert)
       // descriptor bases; K-steps advance the start address (+32 B = +2 encoded)
       const uint64_t dK0 = make_sdesc_sw128(smem_u32(sK), 16, 1024), dV0 = make_sdesc_sw128(smem_u32(sV), 16, 1024);
       const uint64_t dG0 = make_sdesc_sw128(aG, 16, 1024);
       GranSeq<NG> seq;
-      int gq[2], go[2];  // granules of Q / dO of the pairs in flight (by pair parity)
+      // granules of Q / dO of the two pairs in flight, by pair parity (scalars: a
+      // runtime-indexed array would live in local memory, whose loads the SS MMA
+      // operand stream starves). The issuing warp runs nearly in lock-step with the
+      // tensor pipe, so everything between two product groups is kept minimal.
+      int gq0 = 0, gq1 = 0, go0 = 0, go1 = 0;
       mbar_wait_warp(&sm->kv_full, 0);
       // S(n) = Qpair.K^T and dP(n) = dOpair.V^T into TMEM buffer n&1
       auto issue_s = [&](int n) {
         const int b = n & 1;
         const int g0 = seq.next(2 * n);
-        gq[b] = g0;
-        if (!(tr.ablate & 16)) {
-          if (n >= 2) named_bar_b(kBarSdFree + b, kCompute + 32);
-          named_bar_b(kBarGran + ((2 * n) & 3), 64);
-        }
+        if (b) gq1 = g0; else gq0 = g0;
+        if (n >= 2) named_bar_b(kBarSdFree + b, kCompute + 32);
+        named_bar_b(kBarGran, 64);
         tc_fence_after();
-        if (lane == 0) trace_ev(tr, 14, n);
         const uint64_t q0 = dG0 + uint64_t((g0 * C::kGran) >> 4);
 #pragma unroll
-        for (int s = 0; s < D / 16; ++s) {
+        for (int s = 0; s < D / 16; ++s)
           umma_bf16_warp(tbase + b * 64, q0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
                          dK0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
-        }
         umma_commit_warp(&sm->s_full[b]);
-        if (lane == 0) trace_ev(tr, 3, n);
       };
       auto issue_dp = [&](int n) {
         const int b = n & 1;
         const int g1 = seq.next(2 * n + 1);
-        go[b] = g1;
-        if (!(tr.ablate & 16)) named_bar_b(kBarGran + ((2 * n + 1) & 3), 64);
+        if (b) go1 = g1; else go0 = g1;
+        named_bar_b(kBarGran, 64);
         tc_fence_after();
-        if (lane == 0) trace_ev(tr, 15, n);
         const uint64_t o0 = dG0 + uint64_t((g1 * C::kGran) >> 4);
 #pragma unroll
         for (int s = 0; s < D / 16; ++s)
           umma_bf16_warp(tbase + 128 + b * 64, o0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
                          dV0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
         umma_commit_warp(&sm->dp_full[b]);
-        if (lane == 0) trace_ev(tr, 13, n);
       };
+      const uint64_t dP0 = make_sdesc_sw128(aP, 8192, 1024), dS0 = make_sdesc_sw128(aS, 8192, 1024);
+      const uint32_t lboZ = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - aG;  // minus granule offset
       // Fixed software-pipelined order per pair p:  S(p+1), dV(p), dP(p+1), dK(p).
       // The exp / dS math of a pair runs a full period ahead of its dV / dK, and the
       // granule of dO(p) is released (after dV(p)) early enough to refill dO(p+2)
@@ -392,37 +390,34 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       issue_s(0);
       issue_dp(0);
       for (int p = 0; p < npairs; ++p) {
-        const int b = p & 1, pb = p % NPB;
+        const int b = p & 1;
         if (p + 1 < npairs) issue_s(p + 1);
-        if (!(tr.ablate & 16)) named_bar_b(kBarPFull, kCompute + 32);
+        named_bar_b(kBarPFull, kCompute + 32);
         tc_fence_after();
         if (lane == 0) trace_ev(tr, 1, p);
         {
-          const uint32_t o0 = aG + go[b] * C::kGran;
-          const uint32_t lbo = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - o0;
-          const uint64_t da = make_sdesc_sw128(o0, lbo, 1024), db = make_sdesc_sw128(aP + pb * 16384, 8192, 1024);
+          const int g = b ? go1 : go0;
+          const uint32_t goff = uint32_t(g * C::kGran);
+          const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_bf16_warp(tbase + 256, da + uint64_t(s * 128), db + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+            umma_bf16_warp(tbase + 256, da + uint64_t(s * 128), dP0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+          umma_commit_warp(&sm->g_empty[g]);
         }
-        umma_commit_warp(&sm->g_empty[go[b]]);
-        umma_commit_warp(&sm->p_empty[pb]);
-        if (lane == 0) trace_ev(tr, 4, p);
+        umma_commit_warp(&sm->p_empty[0]);
         if (p + 1 < npairs) issue_dp(p + 1);
-        if (!(tr.ablate & 16)) named_bar_b(kBarDsFull, kCompute + 32);
+        named_bar_b(kBarDsFull, kCompute + 32);
         tc_fence_after();
-        if (lane == 0) trace_ev(tr, 0, p);
         {
-          const uint32_t q0 = aG + gq[b] * C::kGran;
-          const uint32_t lbo = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - q0;
-          const uint64_t da = make_sdesc_sw128(q0, lbo, 1024), db = make_sdesc_sw128(aS + pb * 16384, 8192, 1024);
+          const int g = b ? gq1 : gq0;
+          const uint32_t goff = uint32_t(g * C::kGran);
+          const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_bf16_warp(tbase + 320, da + uint64_t(s * 128), db + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+            umma_bf16_warp(tbase + 320, da + uint64_t(s * 128), dS0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+          umma_commit_warp(&sm->g_empty[g]);
         }
-        umma_commit_warp(&sm->g_empty[gq[b]]);
-        umma_commit_warp(&sm->ds_empty[pb]);
-        if (lane == 0) trace_ev(tr, 12, p);
+        umma_commit_warp(&sm->ds_empty[0]);
       }
       umma_commit_warp(&sm->final_bar);
     }
@@ -440,7 +435,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     } else if (threadIdx.x < D + 64) {
       sm->rows[threadIdx.x - D] = cube_out_row(L, u, kc, threadIdx.x - D, raster);
     }
-    for (int p = 0; p < ((tr.ablate & 16) ? 0 : npairs); ++p) {
+    for (int p = 0; p < npairs; ++p) {
       const int b = p & 1, pb = p % NPB, use = p / NPB;
       uint8_t* myP = sP + pb * 16384;
       uint8_t* myS = sS + pb * 16384;
@@ -457,12 +452,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       tc_fence_after();
       float pf[32];
       uint32_t pk[16];
-      if (tr.ablate & 1) {  // debug: no TMEM load, no exp
-#pragma unroll
-        for (int j = 0; j < 32; ++j) pf[j] = lse2 * 1e-30f;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = 0u;
-      } else {
+      {
         uint32_t rs[32];
         tmem_ld32_raw(lrow + b * 64 + ch * 32, rs);
         tmem_wait_ld();
@@ -483,10 +473,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       mbar_wait_sleep(&sm->dp_full[b], (p >> 1) & 1);
       if (threadIdx.x == 0) trace_ev(tr, 9, p);
       tc_fence_after();
-      if (tr.ablate & 1) {
-        tc_fence_before();
-        named_bar_arrive(kBarSdFree + b, kCompute + 32);
-      } else {
+      {
         uint32_t rd[32];
         tmem_ld32_raw(lrow + 128 + b * 64 + ch * 32, rd);
         tmem_wait_ld();
@@ -500,7 +487,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       if (threadIdx.x == 0) trace_ev(tr, 10, p);
       if (p >= NPB) {
         mbar_wait_sleep(&sm->ds_empty[pb], (use - 1) & 1);                 // dK of the previous user done
-        if (ds_store && !(tr.ablate & 2)) mbar_wait_sleep(&sm->ds_stored[pb], (use - 1) & 1);  // and its dS store read it
+        if (ds_store) mbar_wait_sleep(&sm->ds_stored[pb], (use - 1) & 1);  // and its dS store read it
       }
       if (threadIdx.x == 0) trace_ev(tr, 11, p);
 #pragma unroll

@@ -35,15 +35,13 @@ for cta in (300, 301):
     b = buf.cpu().tolist()
     ev = {(i // 256, i % 256): b[i] for i in range(cap) if b[i] != 0}
     t0 = ev.get((24, 0), min(ev.values()))
-    cols = [("ldQ", 2, lambda p: 2 * p), ("ldO", 2, lambda p: 2 * p + 1), ("S0", 14, None), ("S", 3, None),
-            ("dP0", 15, None), ("dP", 13, None), ("dV0", 1, None), ("dK0", 0, None),
+    cols = [("ldQ", 2, lambda p: 2 * p), ("ldO", 2, lambda p: 2 * p + 1), ("dV0", 1, None),
             ("gotS", 5, None), ("Prdy", 6, None), ("Pbuf", 8, None), ("gotdP", 9, None), ("dSrdy", 10, None),
-            ("dSbuf", 11, None), ("done", 7, None), ("dV", 4, None), ("dK", 12, None), ("xS", 16, None),
-            ("xdP", 17, None), ("xdV", 18, None), ("xdK", 19, None)]
+            ("dSbuf", 11, None), ("done", 7, None), ("xS", 16, None)]
     print(f"=== dkdv cta {cta}: {len(ev)} events (cycles from first event; ld = TMA issue, S/dP/dV/dK = MMA issued)")
     print("  p " + "".join(f"{n:>8s}" for n, _, _ in cols))
     names = {0: "entry", 4: "after TMEM alloc", 1: "epilogue start", 2: "epilogue rows written", 3: "exit"}
-    print("  CTA:", {names[i]: ev[(24, i)] - t0 for i in names if (24, i) in ev}, "npairs ~", max(p for (c, p) in ev if c == 3) + 1)
+    print("  CTA:", {names[i]: ev[(24, i)] - t0 for i in names if (24, i) in ev}, "npairs ~", max([p for (c, p) in ev if c == 1] or [-1]) + 1)
     for p in range(2, 10):
         a, b, c = ev.get((14, p)), ev.get((3, p)), ev.get((16, p))
         if None not in (a, b, c):
