@@ -34,12 +34,7 @@ int cuda_status(cudaError_t e, const char* where) {
 static std::atomic<uint64_t> g_launches{0};
 static vsa_dev::TraceCfg g_trace{nullptr, 0, 0, 0};
 
-vsa_dev::TraceCfg debug_trace() {
-  vsa_dev::TraceCfg t = g_trace;
-  const char* e = getenv("VSA_ABLATE");
-  t.ablate = e ? atoi(e) : 0;
-  return t;
-}
+vsa_dev::TraceCfg debug_trace() { return g_trace; }
 
 int kernel_status(const char* where) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -91,7 +86,7 @@ const char* vsa_version(void) { return "vsa_b200 0.1 (sm_100a)"; }
 uint64_t vsa_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int vsa_debug_trace(void* buf, int32_t cap, int32_t cta_x, int32_t cta_y) {
-  g_trace = vsa_dev::TraceCfg{static_cast<unsigned long long*>(buf), cap, cta_x, cta_y, 0};
+  g_trace = vsa_dev::TraceCfg{static_cast<unsigned long long*>(buf), cap, cta_x, cta_y};
   return VSA_OK;
 }
 

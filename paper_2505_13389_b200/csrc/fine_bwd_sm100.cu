@@ -44,6 +44,9 @@ __device__ __forceinline__ float ex2b(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// (No FMA-pipe exp offload here, unlike the forward: the compute warps share SMSPs
+// with the MMA-issuing warp, and the extra FMA-pipe instructions slowed the dK/dV
+// pass by ~10% — the issuer is more sensitive to issue-slot pressure than MUFU.)
 __device__ __forceinline__ void named_bar_b(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -358,10 +361,10 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int b = n & 1;
         const int g0 = seq.next(2 * n);
         if (b) gq1 = g0; else gq0 = g0;
+        const uint64_t q0 = dG0 + uint64_t((g0 * C::kGran) >> 4);
         if (n >= 2) named_bar_b(kBarSdFree + b, kCompute + 32);
         named_bar_b(kBarGran, 64);
         tc_fence_after();
-        const uint64_t q0 = dG0 + uint64_t((g0 * C::kGran) >> 4);
 #pragma unroll
         for (int s = 0; s < D / 16; ++s)
           umma_bf16_warp(tbase + b * 64, q0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
@@ -372,9 +375,9 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int b = n & 1;
         const int g1 = seq.next(2 * n + 1);
         if (b) go1 = g1; else go0 = g1;
+        const uint64_t o0 = dG0 + uint64_t((g1 * C::kGran) >> 4);
         named_bar_b(kBarGran, 64);
         tc_fence_after();
-        const uint64_t o0 = dG0 + uint64_t((g1 * C::kGran) >> 4);
 #pragma unroll
         for (int s = 0; s < D / 16; ++s)
           umma_bf16_warp(tbase + 128 + b * 64, o0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
@@ -392,13 +395,12 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       for (int p = 0; p < npairs; ++p) {
         const int b = p & 1;
         if (p + 1 < npairs) issue_s(p + 1);
-        named_bar_b(kBarPFull, kCompute + 32);
-        tc_fence_after();
-        if (lane == 0) trace_ev(tr, 1, p);
         {
           const int g = b ? go1 : go0;
           const uint32_t goff = uint32_t(g * C::kGran);
           const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
+          named_bar_b(kBarPFull, kCompute + 32);
+          tc_fence_after();
 #pragma unroll
           for (int s = 0; s < 8; ++s)
             umma_bf16_warp(tbase + 256, da + uint64_t(s * 128), dP0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
@@ -406,12 +408,12 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         }
         umma_commit_warp(&sm->p_empty[0]);
         if (p + 1 < npairs) issue_dp(p + 1);
-        named_bar_b(kBarDsFull, kCompute + 32);
-        tc_fence_after();
         {
           const int g = b ? gq1 : gq0;
           const uint32_t goff = uint32_t(g * C::kGran);
           const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
+          named_bar_b(kBarDsFull, kCompute + 32);
+          tc_fence_after();
 #pragma unroll
           for (int s = 0; s < 8; ++s)
             umma_bf16_warp(tbase + 320, da + uint64_t(s * 128), dS0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
@@ -435,18 +437,27 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     } else if (threadIdx.x < D + 64) {
       sm->rows[threadIdx.x - D] = cube_out_row(L, u, kc, threadIdx.x - D, raster);
     }
+    // lse / delta of this thread's query row, prefetched one pair ahead (two dependent
+    // global loads per pair would otherwise sit on the compute path)
+    auto row_stats = [&](int pp, float& l2, float& dlt) {
+      l2 = 0.f;
+      dlt = 0.f;
+      if (pp < npairs && (ql < 64 || 2 * pp + 1 < nq)) {
+        const int qcube = list[beg + 2 * pp + (ql >> 6)];
+        const int64_t trow = int64_t(row0) + int64_t(qcube) * 64 + (ql & 63);
+        l2 = lse[trow];
+        dlt = delta[trow];
+      }
+    };
+    float nl2, ndl;
+    row_stats(0, nl2, ndl);
     for (int p = 0; p < npairs; ++p) {
       const int b = p & 1, pb = p % NPB, use = p / NPB;
       uint8_t* myP = sP + pb * 16384;
       uint8_t* myS = sS + pb * 16384;
       const bool valid = ql < 64 || (2 * p + 1 < nq);  // warp-uniform
-      float lse2 = 0.f, dl = 0.f;
-      if (valid) {
-        const int qcube = list[beg + 2 * p + (ql >> 6)];
-        const int64_t trow = int64_t(row0) + int64_t(qcube) * 64 + (ql & 63);
-        lse2 = lse[trow] * 1.4426950408889634f;
-        dl = delta[trow];
-      }
+      const float lse2 = nl2 * 1.4426950408889634f, dl = ndl;
+      row_stats(p + 1, nl2, ndl);
       mbar_wait_sleep(&sm->s_full[b], (p >> 1) & 1);
       if (threadIdx.x == 0) trace_ev(tr, 5, p);
       tc_fence_after();
@@ -457,7 +468,14 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         tmem_ld32_raw(lrow + b * 64 + ch * 32, rs);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) pf[j] = valid ? ex2b(fmaf(__uint_as_float(rs[j]), scale_log2, -lse2)) : 0.f;
+        for (int j = 0; j < 16; ++j) {
+          float a, c;
+          f2_unpack(ffma2(f2(__uint_as_float(rs[2 * j]), __uint_as_float(rs[2 * j + 1])), f2(scale_log2, scale_log2),
+                          f2(-lse2, -lse2)),
+                    a, c);
+          pf[2 * j] = valid ? ex2b(a) : 0.f;
+          pf[2 * j + 1] = valid ? ex2b(c) : 0.f;
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(pf[2 * j], pf[2 * j + 1]);
       }
@@ -481,8 +499,13 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         named_bar_arrive(kBarSdFree + b, kCompute + 32);
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          pk[j] = pack_bf16(pf[2 * j] * (__uint_as_float(rd[2 * j]) - dl),
-                            pf[2 * j + 1] * (__uint_as_float(rd[2 * j + 1]) - dl));
+        {
+          float a, c;
+          f2_unpack(fmul2(f2(pf[2 * j], pf[2 * j + 1]),
+                          fadd2(f2(__uint_as_float(rd[2 * j]), __uint_as_float(rd[2 * j + 1])), f2(-dl, -dl))),
+                    a, c);
+          pk[j] = pack_bf16(a, c);
+        }
       }
       if (threadIdx.x == 0) trace_ev(tr, 10, p);
       if (p >= NPB) {

@@ -100,6 +100,10 @@ __device__ __forceinline__ float ex2(float x) {
 // x = n + f, f in [-0.5, 0.5], degree-3 fit of 2^f (max rel. error 7.7e-5, far
 // below the bf16 rounding of P), 2^n added into the exponent field. Inputs are
 // clamped at -120 (2^-120 ~ 0 next to the running max's 2^0).
+#ifndef VSA_FWD_POLY_EXP
+#define VSA_FWD_POLY_EXP 0
+#endif
+constexpr bool kPolyExp = VSA_FWD_POLY_EXP != 0;
 __device__ __forceinline__ float ex2_poly(float x) {
   x = fmaxf(x, -120.f);
   const float t = x + 12582912.f;  // 1.5 * 2^23: rint(x) in the low mantissa bits
@@ -291,12 +295,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // (cube, pair) kept as incremental counters, descriptors by additions.
       auto issue_s = [&](int gp, int j, int p) {
         const int qb = j & 1;
+        const int g = (2 * gp) & (NG - 1);
+        const uint64_t a0 = dG0 + uint64_t((g * C::kGran) >> 4), b0 = dQ0 + uint64_t((qb * C::kQBytes) >> 4);
         if (p == 0) mbar_wait_warp(&sm->q_full[qb], (j >> 1) & 1);
         if (gp >= 2) named_bar(kFbSFree + (gp & 1), 288);
         named_bar(kFbGran, 64);  // K(gp) landed
         tc_fence_after();
-        const int g = (2 * gp) & (NG - 1);
-        const uint64_t a0 = dG0 + uint64_t((g * C::kGran) >> 4), b0 = dQ0 + uint64_t((qb * C::kQBytes) >> 4);
 #pragma unroll
         for (int s = 0; s < D / 16; ++s)
           umma_bf16_warp(tbase + (gp & 1) * 64, a0 + (((s >> 2) * C::kChunkStride + (s & 3) * 32) >> 4),
@@ -316,15 +320,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (++sp == np) sp = 0, ++sj;
         }
         const int tb = j & 1;
-        named_bar(kFbGran, 64);                               // V(gp) landed
-        named_bar(kFbPFull + (gp & 1), 288);                  // P^T(gp) written
-        if (p == 0 && j >= 2) named_bar(kFbOFree + tb, 160);  // O^T[tb] read by the epilogue of cube j-2
-        tc_fence_after();
-        if (lane == 0) trace_ev(tr, 5, gp);
         const int g = (2 * gp + 1) & (NG - 1);
         const uint32_t goff = uint32_t(g * C::kGran);
         const uint64_t a0 = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
         const uint64_t b0 = dP0 + uint64_t(((gp & 1) * 16384) >> 4);
+        named_bar(kFbGran, 64);                               // V(gp) landed
+        named_bar(kFbPFull + (gp & 1), 288);                  // P^T(gp) written
+        if (p == 0 && j >= 2) named_bar(kFbOFree + tb, 160);  // O^T[tb] read by the epilogue of cube j-2
+        tc_fence_after();
 #pragma unroll
         for (int s = 0; s < 8; ++s)
           umma_bf16_warp(tbase + 128 + tb * 64, a0 + uint64_t(s * 128), b0 + uint64_t(s * 128), idO,
@@ -378,9 +381,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (threadIdx.x == 0) trace_ev(tr, 9, gp);
         float mx = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          x[i] = fmaf(x[i], scale_log2, -mreg[i]);
-          mx = fmaxf(mx, x[i]);
+        for (int i = 0; i < 32; i += 2) {
+          f2_unpack(ffma2(f2(x[i], x[i + 1]), f2(scale_log2, scale_log2), f2(-mreg[i], -mreg[i + 1])), x[i], x[i + 1]);
+          mx = fmaxf(mx, fmaxf(x[i], x[i + 1]));
         }
         const bool upd = named_bar_or(barSoft, 128, valid && mx > tau);  // `valid` is warp-uniform
         if (threadIdx.x == 0) trace_ev(tr, 10, gp);
@@ -456,9 +459,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int i = 0; i < 16; ++i) {
             // half of the exponentials on MUFU, half as a polynomial on the FMA pipe
             const float p0 = ex2(x[2 * i]);
-            const float p1 = ex2_poly(x[2 * i + 1]);
-            lsum[2 * i] += p0;
-            lsum[2 * i + 1] += p1;
+            const float p1 = kPolyExp ? ex2_poly(x[2 * i + 1]) : ex2(x[2 * i + 1]);
+            f2_unpack(fadd2(f2(lsum[2 * i], lsum[2 * i + 1]), f2(p0, p1)), lsum[2 * i], lsum[2 * i + 1]);
             pk[i] = pack_bf16(p0, p1);
           }
 #pragma unroll

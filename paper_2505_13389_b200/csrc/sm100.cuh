@@ -40,12 +40,18 @@ __device__ __forceinline__ bool elect_one() {
 struct TraceCfg {
   unsigned long long* buf;
   int cap, cta_x, cta_y;
-  int ablate;  // debug-only timing ablations (VSA_ABLATE env), 0 in normal runs
 };
+// Compiled in only with -DVSA_TRACE (tools/trace_*.py rebuild with it): even a
+// disabled probe costs a constant-bank load, a clock read and a branch, which the
+// MMA-issuing warps pay in lock-step with the tensor pipe.
 __device__ __forceinline__ void trace_ev(const TraceCfg& t, int code, int idx) {
+#ifdef VSA_TRACE
   if (t.buf != nullptr && int(blockIdx.x) == t.cta_x && int(blockIdx.y) == t.cta_y && idx < 256 &&
       code * 256 + idx < t.cap)
     t.buf[code * 256 + idx] = clock64();
+#else
+  (void)t, (void)code, (void)idx;
+#endif
 }
 
 // ---------------------------------------------------------------- mbarrier
@@ -288,6 +294,32 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
 // XOR-ed with (row % 8).
 __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t byte_in_row) {
   return row * 128u + ((((byte_in_row >> 4) ^ (row & 7u)) << 4) | (byte_in_row & 15u));
+}
+
+// Packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100a): half the issue slots
+// of the elementwise softmax / dS math, which shares SMSPs with the MMA issuer.
+__device__ __forceinline__ uint64_t f2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
