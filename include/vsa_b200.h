@@ -194,6 +194,26 @@ size_t vsa_fine_backward_workspace_bytes(const vsa_layout_t* layout, int64_t bh,
 int vsa_unpool_max_add(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled,
                        const float* dxc, int32_t raster, void* dx, void* stream);
 
+/* Replaces: the gate projection of vsa_forward (vsa.hpp:100-112): z = hidden . Wg
+ * (+ bias), optional sigmoid, split into Gc = z[:, h*d:(h+1)*d] and Gf = z[:, (H+h)*d:...]
+ * written as [B, H, S, d] bf16 in the layout's raster I/O order (Gf = 1 in adaptation
+ * mode). hidden: bf16 [B, S, model_dim] (S = t*h*w); weight: bf16 [model_dim, 2*H*d]
+ * row-major; bias: fp32 [2*H*d] or NULL. tcgen05 GEMM (gemm_sm100.cu); needs
+ * model_dim % 64 == 0 and 2*H*d % 256 == 0. */
+int vsa_gate_forward(const vsa_layout_t* layout, int64_t batch, int64_t heads, int64_t d, int64_t model_dim,
+                     const void* hidden, const void* weight, const float* bias, int32_t activation,
+                     int32_t adaptation, void* gc, void* gf, void* stream);
+/* Replaces: the gate part of vsa_backward (vsa.hpp:152-176): dz = [dGc, dGf] (times
+ * G(1-G) for sigmoid; the Gf half is 0 in adaptation mode), dhidden = dz . Wg^T (bf16
+ * [B, S, model_dim]), dWg = hidden^T . dz (fp32 [model_dim, 2*H*d]), dbias = column sums
+ * of dz (fp32, NULL to skip). gc/gf are the activated gates of the forward (needed for
+ * sigmoid). Workspace: vsa_gate_backward_workspace_bytes. model_dim % 256 == 0. */
+int vsa_gate_backward(const vsa_layout_t* layout, int64_t batch, int64_t heads, int64_t d, int64_t model_dim,
+                      const void* hidden, const void* weight, const void* gc, const void* gf, const void* dgc,
+                      const void* dgf, int32_t activation, int32_t adaptation, void* dz_workspace, void* dhidden,
+                      float* dweight, float* dbias, void* stream);
+size_t vsa_gate_backward_workspace_bytes(const vsa_layout_t* layout, int64_t batch, int64_t heads, int64_t d);
+
 /* Ulysses resharding copy: dst[i1][i0] = src[i0][i1] over an
  * [n0][n1] grid of contiguous blocks of `block_bytes` (a multiple of 16). With
  * n0 = B*S/P, n1 = P, block = (H/P)*d*elem it packs a sequence shard [B,S/P,H,d]

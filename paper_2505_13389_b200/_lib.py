@@ -34,7 +34,7 @@ EXPORTS = [
     "vsa_tile_pool", "vsa_pool_tiled", "vsa_coarse_forward", "vsa_coarse_bitmap_bytes", "vsa_selection_transpose",
     "vsa_validate_selection", "vsa_fine_forward", "vsa_backward_prologue", "vsa_coarse_backward",
     "vsa_fine_backward", "vsa_fine_backward_workspace_bytes", "vsa_unpool_max_add", "vsa_layout_set_io",
-    "vsa_transpose_blocks",
+    "vsa_transpose_blocks", "vsa_gate_forward", "vsa_gate_backward", "vsa_gate_backward_workspace_bytes",
 ]
 
 
@@ -71,6 +71,9 @@ def lib():
         "vsa_debug_trace": [P, I32, I32, I32],
         "vsa_layout_set_io": [LP, I32, I64, I64, I64],
         "vsa_transpose_blocks": [P, P, I64, I64, I64, P],
+        "vsa_gate_forward": [LP, I64, I64, I64, I64, P, P, P, I32, I32, P, P, P],
+        "vsa_gate_backward": [LP, I64, I64, I64, I64, P, P, P, P, P, P, I32, I32, P, P, P, P, P],
+        "vsa_gate_backward_workspace_bytes": [LP, I64, I64, I64],
         "vsa_flatten_index": [LP, I64, I64, I64, C.POINTER(I64)],
         "vsa_tile": [LP, I64, I64, I32, P, P, P],
         "vsa_untile": [LP, I64, I64, I32, P, P, P],
@@ -94,6 +97,7 @@ def lib():
     L.vsa_coarse_bitmap_bytes.restype = C.c_size_t
     L.vsa_fine_backward_workspace_bytes.argtypes = [LP, I64, I64]
     L.vsa_fine_backward_workspace_bytes.restype = C.c_size_t
+    L.vsa_gate_backward_workspace_bytes.restype = C.c_size_t
     _lib = L
     return L
 

@@ -596,8 +596,8 @@ class VsaHostPipeline:
 # ----------------------------------------------------------------------------- gate projection (vsa.hpp:100-112)
 @dataclass
 class VsaParams:
-    """VsaParams (vsa.hpp:16-52) with torch tensors; the gate projection is a
-    plain library GEMM (SURVEY.md §8 f1 — not one of the six kernels)."""
+    """VsaParams (vsa.hpp:16-52) with torch tensors; the gate projection runs on the
+    tcgen05 GEMM of csrc/gemm_sm100.cu."""
 
     gate_weight: torch.Tensor            # [model_dim, 2*H*d]
     gate_bias: torch.Tensor | None = None
@@ -615,33 +615,64 @@ class VsaParams:
             raise ValueError("VsaParams: k must be >= 1")
 
 
-def gates_from_hidden(hidden: torch.Tensor, params: VsaParams, H: int, d: int):
-    """z = hidden Wg (+b) [sigmoid]; split into Gc, Gf [B,H,S,d] (vsa.hpp:100-112)."""
-    B, _, S, md = hidden.shape
-    z = hidden[:, 0].float() @ params.gate_weight.float()
-    if params.gate_bias is not None and params.gate_bias.numel():
-        z = z + params.gate_bias.float().reshape(1, 1, -1)
-    if params.activation == GATE_SIGMOID:
-        z = torch.sigmoid(z)
-    z = z.view(B, S, 2, H, d).permute(2, 0, 3, 1, 4)
-    gc = z[0].contiguous().to(hidden.dtype)
-    gf = torch.ones_like(gc) if params.adaptation else z[1].contiguous().to(hidden.dtype)
+def _gate_layout(layout, S):
+    if layout is None:
+        return TileLayout(1, 1, S, 1, 1, 1)  # head-major [B,H,S,d] gates, no tiling involved
+    if layout.seq_len != S:
+        raise ValueError("gates: layout sequence length does not match hidden")
+    return layout
+
+
+def _gate_bias(params: VsaParams):
+    if params.gate_bias is None or params.gate_bias.numel() == 0:
+        return None
+    return params.gate_bias.float().contiguous()
+
+
+def gates_from_hidden(hidden: torch.Tensor, params: VsaParams, H: int, d: int, layout=None, op=None):
+    """z = hidden Wg (+b) [sigmoid]; split into Gc, Gf [B,H,S,d] (vsa.hpp:100-112).
+
+    tcgen05 GEMM with the bias / activation / split fused in its epilogue
+    (vsa_gate_forward). hidden: bf16 CUDA [B, 1, S, model_dim]; gate_weight bf16
+    [model_dim, 2*H*d]. With ``op`` (a VsaOp) the gates are written in the op's raster
+    I/O layout (e.g. sequence-major)."""
+    _cuda4(hidden, "hidden")
+    B, one, S, md = hidden.shape
+    if one != 1:
+        raise ValueError("vsa: hidden states are [batch, 1, seq, model_dim]")
+    params.check(md, H, d)
+    w = params.gate_weight
+    if hidden.dtype != torch.bfloat16 or w.dtype != torch.bfloat16 or not w.is_cuda or not w.is_contiguous():
+        raise ValueError("gates: bf16 CUDA hidden and gate_weight required")
+    if op is not None:
+        lref, shape = op._lref, op.io_shape
+    else:
+        lref, shape = _gate_layout(layout, S).ref(), (B, H, S, d)
+    gc = torch.empty(shape, dtype=hidden.dtype, device=hidden.device)
+    gf = torch.empty(shape, dtype=hidden.dtype, device=hidden.device)
+    bias = _gate_bias(params)
+    check(L.lib().vsa_gate_forward(lref, B, H, d, md, _p(hidden), _p(w), _p(bias) if bias is not None else None,
+                                   int(params.activation), 1 if params.adaptation else 0, _p(gc), _p(gf), _stream()))
     return gc, gf
 
 
-def gate_backward(hidden, params: VsaParams, gc, gf, dgc, dgf):
-    """dz -> dhidden, dWg, dbias (vsa.hpp:152-176)."""
+def gate_backward(hidden, params: VsaParams, gc, gf, dgc, dgf, layout=None, op=None):
+    """dz -> dhidden, dWg, dbias (vsa.hpp:152-176) on tcgen05 (vsa_gate_backward):
+    dz = [dGc, dGf] (x G(1-G) for sigmoid), dhidden = dz Wg^T (bf16), dWg = hidden^T dz
+    and dbias = colsum(dz) (fp32)."""
     B, _, S, md = hidden.shape
-    H, d = gc.shape[1], gc.shape[3]
-    dgc, dgf = dgc.float(), dgf.float()
-    if params.activation == GATE_SIGMOID:
-        dgc = dgc * gc.float() * (1 - gc.float())
-        if not params.adaptation:
-            dgf = dgf * gf.float() * (1 - gf.float())
-    if params.adaptation:
-        dgf = torch.zeros_like(dgf)
-    dz = torch.stack([dgc, dgf], 0).permute(1, 3, 0, 2, 4).reshape(B, S, 2 * H * d)
-    dhidden = (dz @ params.gate_weight.float().T).unsqueeze(1).to(hidden.dtype)
-    dW = torch.einsum("bsm,bsn->mn", hidden[:, 0].float(), dz)
-    db = dz.sum(dim=(0, 1)) if params.gate_bias is not None and params.gate_bias.numel() else None
+    d = gc.shape[-1]
+    H = params.gate_weight.shape[1] // (2 * d)
+    lref = op._lref if op is not None else _gate_layout(layout, S).ref()
+    lib = L.lib()
+    wsb = lib.vsa_gate_backward_workspace_bytes(lref, B, H, d)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=hidden.device)
+    dhidden = torch.empty_like(hidden)
+    dW = torch.empty(params.gate_weight.shape, dtype=torch.float32, device=hidden.device)
+    bias = _gate_bias(params)
+    db = torch.empty(bias.shape, dtype=torch.float32, device=hidden.device) if bias is not None else None
+    check(lib.vsa_gate_backward(lref, B, H, d, md, _p(hidden), _p(params.gate_weight), _p(gc), _p(gf), _p(dgc),
+                                _p(dgf) if dgf is not None else None, int(params.activation),
+                                1 if params.adaptation else 0, _p(ws), _p(dhidden), _p(dW),
+                                _p(db) if db is not None else None, _stream()))
     return dhidden, dW, db
