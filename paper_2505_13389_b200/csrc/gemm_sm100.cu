@@ -11,8 +11,10 @@
 //
 // Tile 128 x 256 (cta_group::1, M=128, N=256: a full-rate UMMA — SS operands 12 KB
 // per 128 cycles, under the 128 B/cycle SMEM-operand bound), K staged 64 at a time in
-// a 4-deep TMA ring (48 KB per stage). Warp 0 producer, warp 1 TMEM allocator + MMA
-// issuer (whole warp), warps 4-7 epilogue (TMEM lane quadrant = warp % 4). The
+// a 4-deep TMA ring (48 KB per stage). Persistent (one CTA per SM) with a double-
+// buffered TMEM accumulator. Warp 0 producer, warp 1 TMEM allocator + MMA issuer
+// (whole warp), warps 4-11 epilogue (TMEM lane quadrant = warp % 4, 128 columns
+// each). The
 // epilogue applies bias + activation and writes the gate tensors in the op's layout,
 // a plain bf16 row-major C, or fp32 (weight gradient).
 #include <cmath>
@@ -24,7 +26,7 @@
 
 namespace vsa_dev {
 
-constexpr int kGemmThreads = 256;
+constexpr int kGemmThreads = 384;  // producer, MMA, 2 spare, 8 epilogue warps
 constexpr int kGBM = 128, kGBN = 256, kGBK = 64, kGStages = 4;
 constexpr int kGABytes = kGBM * kGBK * 2;  // 16 KB
 constexpr int kGBBytes = kGBN * kGBK * 2;  // 32 KB
@@ -45,7 +47,7 @@ struct GemmEpi {
 };
 
 struct GemmSmall {
-  uint64_t full[kGStages], empty[kGStages], acc_full;
+  uint64_t full[kGStages], empty[kGStages], acc_full[2], acc_empty[2];
   uint32_t tmem;
 };
 
@@ -53,20 +55,26 @@ template <bool kAMN, bool kBMN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, int M,
                            int N, int K, GemmEpi epi) {
+  // Persistent over output tiles t = blockIdx.x + i*gridDim.x (tn fastest); the
+  // accumulator is double-buffered in TMEM (2 x 256 columns) so the epilogue of tile
+  // i overlaps the MMAs of tile i+1, and the TMA ring runs across tile boundaries.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   GemmSmall* sm = reinterpret_cast<GemmSmall*>(smem + kGStages * kGStage);
   const int warp = int(warp_id()), lane = int(lane_id());
-  const int n0 = int(blockIdx.x) * kGBN, m0 = int(blockIdx.y) * kGBM;
   const int nk = (K + kGBK - 1) / kGBK;
+  const int tiles_n = (N + kGBN - 1) / kGBN, tiles = tiles_n * ((M + kGBM - 1) / kGBM);
 
-  if (warp == 1) tmem_alloc<256>(&sm->tmem);
+  if (warp == 1) tmem_alloc<512>(&sm->tmem);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kGStages; ++s) {
       mbar_init(&sm->full[s], 1);
       mbar_init(&sm->empty[s], 1);
     }
-    mbar_init(&sm->acc_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm->acc_full[b], 1);
+      mbar_init(&sm->acc_empty[b], 256);
+    }
     fence_barrier_init();
   }
   tc_fence_before();
@@ -78,96 +86,128 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       tma_prefetch_desc(&tm_a);
       tma_prefetch_desc(&tm_b);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int st = kb % kGStages;
-        mbar_wait(&sm->empty[st], ((kb / kGStages) & 1) ^ 1);
-        mbar_arrive_expect_tx(&sm->full[st], kGStage);
-        uint8_t* a = smem + st * kGStage;
-        uint8_t* b = a + kGABytes;
-        const int k0 = kb * kGBK;
-        // K-major: box {64 K, rows}; MN-major: boxes {64 MN, 64 K}, one per 64-wide block
-        if (kAMN) {
-          for (int blk = 0; blk < kGBM / 64; ++blk) tma_load_2d(a + blk * 8192, &tm_a, &sm->full[st], m0 + blk * 64, k0);
-        } else {
-          tma_load_2d(a, &tm_a, &sm->full[st], k0, m0);
-        }
-        if (kBMN) {
-          for (int blk = 0; blk < kGBN / 64; ++blk) tma_load_2d(b + blk * 8192, &tm_b, &sm->full[st], n0 + blk * 64, k0);
-        } else {
-          tma_load_2d(b, &tm_b, &sm->full[st], k0, n0);
+      int it = 0;  // global k-block counter (ring position)
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t / tiles_n) * kGBM, n0 = (t % tiles_n) * kGBN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int st = it % kGStages;
+          mbar_wait(&sm->empty[st], ((it / kGStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm->full[st], kGStage);
+          uint8_t* a = smem + st * kGStage;
+          uint8_t* b = a + kGABytes;
+          const int k0 = kb * kGBK;
+          // K-major: box {64 K, rows}; MN-major: boxes {64 MN, 64 K}, one per 64-wide block
+          if (kAMN) {
+            for (int blk = 0; blk < kGBM / 64; ++blk)
+              tma_load_2d(a + blk * 8192, &tm_a, &sm->full[st], m0 + blk * 64, k0);
+          } else {
+            tma_load_2d(a, &tm_a, &sm->full[st], k0, m0);
+          }
+          if (kBMN) {
+            for (int blk = 0; blk < kGBN / 64; ++blk)
+              tma_load_2d(b + blk * 8192, &tm_b, &sm->full[st], n0 + blk * 64, k0);
+          } else {
+            tma_load_2d(b, &tm_b, &sm->full[st], k0, n0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc_bf16(kGBM, kGBN, kAMN, kBMN);
     const uint32_t s0 = smem_u32(smem);
-    for (int kb = 0; kb < nk; ++kb) {
-      const int st = kb % kGStages;
-      mbar_wait_warp(&sm->full[st], (kb / kGStages) & 1);
+    // K-major: rows of 128 B, 8-row atoms at 1024 B, K-step +32 B; MN-major: K rows of
+    // 128 B (64 MN elements), 64-wide MN blocks at 8 KB (LBO), K-step +16 rows = 2 KB
+    const uint64_t ad0 = kAMN ? make_sdesc_sw128(s0, 8192, 1024) : make_sdesc_sw128(s0, 16, 1024);
+    const uint64_t bd0 = kBMN ? make_sdesc_sw128(s0 + kGABytes, 8192, 1024) : make_sdesc_sw128(s0 + kGABytes, 16, 1024);
+    int it = 0, i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int ab = i & 1;
+      if (i >= 2) mbar_wait_warp(&sm->acc_empty[ab], ((i >> 1) - 1) & 1);  // epilogue of tile i-2 read it
       tc_fence_after();
-      const uint32_t a = s0 + st * kGStage, b = a + kGABytes;
-      // K-major: rows of 128 B, 8-row atoms at 1024 B, K-step +32 B; MN-major: K rows of
-      // 128 B (64 MN elements), 64-wide MN blocks at 8 KB (LBO), K-step +16 rows = 2 KB
-      const uint64_t ad = kAMN ? make_sdesc_sw128(a, 8192, 1024) : make_sdesc_sw128(a, 16, 1024);
-      const uint64_t bd = kBMN ? make_sdesc_sw128(b, 8192, 1024) : make_sdesc_sw128(b, 16, 1024);
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int st = it % kGStages;
+        const uint64_t soff = uint64_t((st * kGStage) >> 4);
+        mbar_wait_warp(&sm->full[st], (it / kGStages) & 1);
+        tc_fence_after();
 #pragma unroll
-      for (int s = 0; s < kGBK / 16; ++s)
-        umma_bf16_warp(tbase, ad + uint64_t(kAMN ? s * 128 : s * 2), bd + uint64_t(kBMN ? s * 128 : s * 2), idesc,
-                       (kb > 0 || s > 0) ? 1u : 0u);
-      umma_commit_warp(&sm->empty[st]);
+        for (int s = 0; s < kGBK / 16; ++s)
+          umma_bf16_warp(tbase + ab * kGBN, ad0 + soff + uint64_t(kAMN ? s * 128 : s * 2),
+                         bd0 + soff + uint64_t(kBMN ? s * 128 : s * 2), idesc, (kb > 0 || s > 0) ? 1u : 0u);
+        umma_commit_warp(&sm->empty[st]);
+      }
+      umma_commit_warp(&sm->acc_full[ab]);
     }
-    umma_commit_warp(&sm->acc_full);
   } else if (warp >= 4) {
-    const int q = warp & 3;
-    const int m = m0 + q * 32 + lane;  // this thread's output row
-    const uint32_t lrow = tbase + (uint32_t(q * 32) << 16);
-    mbar_wait(&sm->acc_full, 0);
-    tc_fence_after();
-#pragma unroll 1
-    for (int c0 = 0; c0 < kGBN; c0 += 32) {
-      float v[32];
-      tmem_ld32(lrow + c0, v);
-      const int n = n0 + c0;
-      if (m >= M || n >= N) continue;
+    const int q = warp & 3;            // TMEM lane quadrant
+    const int cbeg = (warp >= 8) ? kGBN / 2 : 0;  // two warps per quadrant, 128 columns each
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int ab = i & 1;
+      const int m0 = (t / tiles_n) * kGBM, n0 = (t % tiles_n) * kGBN;
+      const int m = m0 + q * 32 + lane;  // this thread's output row
+      const uint32_t lrow = tbase + (uint32_t(q * 32) << 16) + ab * kGBN;
+      int gb = 0, gs = 0;  // EPI_GATES: (batch, token) of row m, one division per tile
       if (epi.kind == EPI_GATES) {
-        if (epi.bias) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += epi.bias[n + i];
+        gb = m / epi.S;
+        gs = m - gb * epi.S;
+      }
+      mbar_wait_sleep(&sm->acc_full[ab], (i >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = cbeg; c0 < cbeg + kGBN / 2; c0 += 32) {
+        float v[32];
+        tmem_ld32(lrow + c0, v);
+        if (c0 == cbeg + kGBN / 2 - 32) {  // this warp's columns of the buffer are in registers
+          tc_fence_before();
+          mbar_arrive(&sm->acc_empty[ab]);
         }
-        if (epi.activation == VSA_GATE_SIGMOID) {
+        const int n = n0 + c0;
+        if (m >= M || n >= N) continue;
+        if (epi.kind == EPI_GATES) {
+          if (epi.bias) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 1.0f / (1.0f + __expf(-v[i]));
+            for (int j = 0; j < 32; j += 4) {
+              const float4 b4 = *reinterpret_cast<const float4*>(epi.bias + n + j);
+              v[j] += b4.x;
+              v[j + 1] += b4.y;
+              v[j + 2] += b4.z;
+              v[j + 3] += b4.w;
+            }
+          }
+          if (epi.activation == VSA_GATE_SIGMOID) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __frcp_rn(1.0f + __expf(-v[j]));
+          }
+          const int hd = epi.H * epi.d;
+          const int part = n >= hd ? 1 : 0, nn = n - part * hd, h = nn / epi.d, dd = nn - h * epi.d;
+          if (part == 1 && epi.adaptation) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 1.f;
+          }
+          const int64_t row = raster_row(epi.L, int64_t(gb) * epi.H + h, gs);
+          __nv_bfloat16* dst = (part ? epi.gf : epi.gc) + row * epi.d + dd;
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            float w[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) w[x] = v[j + x];
+            store16(dst + j, w);
+          }
+        } else if (epi.kind == EPI_BF16) {
+          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(epi.c) + int64_t(m) * N + n;
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            float w[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) w[x] = v[j + x];
+            store16(dst + j, w);
+          }
+        } else {
+          float* dst = static_cast<float*>(epi.c) + int64_t(m) * N + n;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
-        const int hd = epi.H * epi.d;
-        const int part = n / hd, h = (n - part * hd) / epi.d, dd = n - part * hd - h * epi.d;
-        if (part == 1 && epi.adaptation) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 1.f;
-        }
-        const int b = m / epi.S, s = m - b * epi.S;
-        const int64_t u = int64_t(b) * epi.H + h;
-        const int64_t row = raster_row(epi.L, u, s);
-        __nv_bfloat16* dst = (part ? epi.gf : epi.gc) + row * epi.d + dd;
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          float w[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) w[t] = v[i + t];
-          store16(dst + i, w);
-        }
-      } else if (epi.kind == EPI_BF16) {
-        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(epi.c) + int64_t(m) * N + n;
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          float w[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) w[t] = v[i + t];
-          store16(dst + i, w);
-        }
-      } else {
-        float* dst = static_cast<float*>(epi.c) + int64_t(m) * N + n;
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
       }
     }
   }
@@ -175,7 +215,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<256>(tbase);
+    tmem_dealloc<512>(tbase);
   }
 }
 
@@ -254,8 +294,11 @@ static int gemm_launch(const void* a, const void* b, int M, int N, int K, const 
   const size_t smem = kGStages * kGStage + sizeof(GemmSmall) + 1024;
   auto kern = gemm_bf16_sm100_kernel<kAMN, kBMN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  dim3 grid(unsigned((N + kGBN - 1) / kGBN), unsigned((M + kGBM - 1) / kGBM));
-  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, M, N, K, epi);
+  const int64_t tiles = int64_t((N + kGBN - 1) / kGBN) * ((M + kGBM - 1) / kGBM);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  kern<<<unsigned(std::min<int64_t>(tiles, sms)), kGemmThreads, smem, st>>>(ta, tb, M, N, K, epi);
   VSA_LAUNCH_CHECK("gemm_bf16_sm100_kernel");
 }
 
