@@ -58,7 +58,7 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
 // bar.arrive (compute warps) / bar.sync (issuer); TMA completions are turned into
 // named-barrier rendezvous by a watcher warp. Each ID carries one event kind in
 // strict order (a producer cannot arrive twice before the issuer syncs: see the
-// p_empty / ds_empty waits), sd_free alternates by pair parity, and the granule
+// waits for the P / dS buffers' release), sd_free alternates by pair parity, and the granule
 // rendezvous is a bar.sync on both sides (pairs up in order on one ID).
 constexpr int kBarPFull = 2, kBarDsFull = 3, kBarSdFree = 4 /* 4,5 */, kBarGran = 6;
 
@@ -196,7 +196,7 @@ struct KVSmall {
   uint64_t kv_full, final_bar;
   uint64_t g_full[10], g_empty[10];
   uint64_t s_full[2], dp_full[2], sd_free[2];
-  uint64_t p_full[2], p_empty[2], ds_full[2], ds_empty[2], ds_stored[2];
+  uint64_t p_full[2], ds_full[2], ds_stored[2];
   uint32_t tmem;
 };
 
@@ -248,9 +248,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     }
     for (int b = 0; b < NPB; ++b) {
       mbar_init(&sm->p_full[b], kCompute);
-      mbar_init(&sm->p_empty[b], 1);
       mbar_init(&sm->ds_full[b], kCompute);
-      mbar_init(&sm->ds_empty[b], 1);
       mbar_init(&sm->ds_stored[b], 1);
     }
     fence_barrier_init();
@@ -406,7 +404,6 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             umma_bf16_warp(tbase + 256, da + uint64_t(s * 128), dP0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
           umma_commit_warp(&sm->g_empty[g]);
         }
-        umma_commit_warp(&sm->p_empty[0]);
         if (p + 1 < npairs) issue_dp(p + 1);
         {
           const int g = b ? gq1 : gq0;
@@ -419,7 +416,6 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             umma_bf16_warp(tbase + 320, da + uint64_t(s * 128), dS0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
           umma_commit_warp(&sm->g_empty[g]);
         }
-        umma_commit_warp(&sm->ds_empty[0]);
       }
       umma_commit_warp(&sm->final_bar);
     }
@@ -451,7 +447,19 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     };
     float nl2, ndl;
     row_stats(0, nl2, ndl);
+    // The P / dS buffers of pair p-1 are free once dV(p-1) / dK(p-1) complete, which is
+    // exactly when the granules of dO(p-1) / Q(p-1) are released: wait on those g_empty
+    // phases (same GranSeq as producer / issuer) instead of extra per-pair commits.
+    GranSeq<NG> gseq;
+    uint32_t uses = 0;           // bit g: parity of the fills of granule g so far
+    int pq_g = 0, po_g = 0;      // granules of Q(p-1), dO(p-1)
+    uint32_t pq_par = 0, po_par = 0;
     for (int p = 0; p < npairs; ++p) {
+      const int cq_g = gseq.next(2 * p), co_g = gseq.next(2 * p + 1);
+      const uint32_t cq_par = (uses >> cq_g) & 1u;
+      uses ^= 1u << cq_g;
+      const uint32_t co_par = (uses >> co_g) & 1u;
+      uses ^= 1u << co_g;
       const int b = p & 1, pb = p % NPB, use = p / NPB;
       uint8_t* myP = sP + pb * 16384;
       uint8_t* myS = sS + pb * 16384;
@@ -480,7 +488,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(pf[2 * j], pf[2 * j + 1]);
       }
       if (threadIdx.x == 0) trace_ev(tr, 6, p);
-      if (p >= NPB) mbar_wait_sleep(&sm->p_empty[pb], (use - 1) & 1);  // dV of the previous user done
+      if (p >= 1) mbar_wait_sleep(&sm->g_empty[po_g], po_par);  // dV(p-1) done: P buffer free
       if (threadIdx.x == 0) trace_ev(tr, 8, p);
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -509,7 +517,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       }
       if (threadIdx.x == 0) trace_ev(tr, 10, p);
       if (p >= NPB) {
-        mbar_wait_sleep(&sm->ds_empty[pb], (use - 1) & 1);                 // dK of the previous user done
+        mbar_wait_sleep(&sm->g_empty[pq_g], pq_par);                       // dK(p-1) done: dS buffer free
         if (ds_store) mbar_wait_sleep(&sm->ds_stored[pb], (use - 1) & 1);  // and its dS store read it
       }
       if (threadIdx.x == 0) trace_ev(tr, 11, p);
@@ -521,6 +529,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       named_bar_arrive(kBarDsFull, kCompute + 32);
       mbar_arrive(&sm->ds_full[pb]);  // for the dS store warp
       if (threadIdx.x == 0) trace_ev(tr, 7, p);
+      pq_g = cq_g, pq_par = cq_par, po_g = co_g, po_par = co_par;
     }
     // ---------------------------------------------------------------- epilogue
     float* stK = reinterpret_cast<float*>(sG);                 // [64][D] fp32
