@@ -358,12 +358,13 @@ int launch_coarse_backward(const vsa_layout_t& L, int64_t bh, int64_t d, const f
   coarse_bwd_ds_kernel<<<unsigned((bh * nc + 3) / 4), 128, 0, st>>>(bh * nc, nc, scale, ac, scratch);
   rc = kernel_status("coarse_bwd_ds_kernel");
   if (rc) return rc;
-  // dQc = dS Kc, dKc = dS^T Qc, dVc = Ac^T dOc
-  rc = launch_gemm_f32(B, nc, D, nc, scratch, snn, nc, 1, kc, snd, D, 1, dqc, snd, D, nullptr, st);
-  if (rc) return rc;
-  rc = launch_gemm_f32(B, nc, D, nc, scratch, snn, 1, nc, qc, snd, D, 1, dkc, snd, D, nullptr, st);
-  if (rc) return rc;
-  return launch_gemm_f32(B, nc, D, nc, ac, snn, 1, nc, doc_cube, snd, D, 1, dvc, snd, D, nullptr, st);
+  // dQc = dS Kc, dKc = dS^T Qc, dVc = Ac^T dOc: one grouped launch (3 x 240 tiles at 1.3B)
+  const GemmF32Args g[3] = {
+      {nc, D, nc, scratch, snn, nc, 1, kc, snd, D, 1, dqc, snd, D, 1.f, 0},
+      {nc, D, nc, scratch, snn, 1, nc, qc, snd, D, 1, dkc, snd, D, 1.f, 0},
+      {nc, D, nc, ac, snn, 1, nc, doc_cube, snd, D, 1, dvc, snd, D, 1.f, 0},
+  };
+  return launch_gemm_f32_grouped(3, g, B, st);
 }
 
 int launch_unpool_max_add(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled,

@@ -10,29 +10,35 @@
 // backward (coarse.hpp:154-162) without copies; tile loads are coalesced along
 // whichever dimension is unit-stride. 64x64 output tile, 16-deep k slab,
 // 256 threads x (4x4) register block, double-buffered smem.
-#include "common.cuh"
 #include "launch.h"
+#include "common.cuh"
 
 namespace vsa_dev {
 
-struct GemmArgs {
-  int M, N, K;
-  const float* A;
-  int64_t sAb, sAm, sAk;
-  const float* B;
-  int64_t sBb, sBk, sBn;
-  float* C;
-  int64_t sCb, sCm;
-  float alpha;
-  int use_alpha;
-};
+using GemmArgs = vsa_host::GemmF32Args;  // launch.h
 
 constexpr int kGT = 64, kGK = 16;
 
-__global__ void __launch_bounds__(256) gemm_f32_kernel(GemmArgs g) {
+// Up to 3 independent products of the same shape in one launch (blockIdx.z = group *
+// batch + b): the three N = d products of the coarse backward fill the GPU together
+// where each alone is 2 x 10 x 12 = 240 tiles. Same canonical per-element order.
+struct GemmGroup {
+  GemmArgs g[3];
+  int batch;
+};
+
+__device__ __forceinline__ void gemm_f32_tile(const GemmArgs& g, int b);
+
+__global__ void __launch_bounds__(256) gemm_f32_kernel(GemmArgs g) { gemm_f32_tile(g, blockIdx.z); }
+
+__global__ void __launch_bounds__(256) gemm_f32_grouped_kernel(const __grid_constant__ GemmGroup gg) {
+  const int grp = blockIdx.z / gg.batch;
+  gemm_f32_tile(gg.g[grp], blockIdx.z - grp * gg.batch);
+}
+
+__device__ __forceinline__ void gemm_f32_tile(const GemmArgs& g, int b) {
   __shared__ __align__(16) float As[2][kGK][kGT + 4];
   __shared__ __align__(16) float Bs[2][kGK][kGT + 4];
-  const int b = blockIdx.z;
   const int m0 = blockIdx.y * kGT, n0 = blockIdx.x * kGT;
   const float* A = g.A + b * g.sAb;
   const float* Bm = g.B + b * g.sBb;
@@ -112,6 +118,16 @@ int launch_gemm_f32(int batch, int M, int N, int K, const float* A, int64_t sAb,
   dim3 grid((N + kGT - 1) / kGT, (M + kGT - 1) / kGT, batch);
   gemm_f32_kernel<<<grid, 256, 0, st>>>(g);
   VSA_LAUNCH_CHECK("gemm_f32_kernel");
+}
+
+int launch_gemm_f32_grouped(int ngroups, const GemmArgs* args, int batch, cudaStream_t st) {
+  GemmGroup gg{};
+  for (int i = 0; i < ngroups; ++i) gg.g[i] = args[i];
+  gg.batch = batch;
+  const int M = args[0].M, N = args[0].N;
+  dim3 grid((N + kGT - 1) / kGT, (M + kGT - 1) / kGT, batch * ngroups);
+  gemm_f32_grouped_kernel<<<grid, 256, 0, st>>>(gg);
+  VSA_LAUNCH_CHECK("gemm_f32_grouped_kernel");
 }
 
 }  // namespace vsa_host

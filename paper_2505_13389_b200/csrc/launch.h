@@ -10,6 +10,21 @@
 
 namespace vsa_host {
 
+// One batched fp32 GEMM C[b] = A[b] . B[b] (alpha) with element strides (gemm_simt.cu).
+struct GemmF32Args {
+  int M, N, K;
+  const float* A;
+  int64_t sAb, sAm, sAk;
+  const float* B;
+  int64_t sBb, sBk, sBn;
+  float* C;
+  int64_t sCb, sCm;
+  float alpha;
+  int use_alpha;
+};
+// Up to 3 same-shape products in one launch (one canonical fma chain per element).
+int launch_gemm_f32_grouped(int ngroups, const GemmF32Args* args, int batch, cudaStream_t st);
+
 // debug event trace target (vsa_debug_trace); buf == nullptr when disabled
 vsa_dev::TraceCfg debug_trace();
 
