@@ -243,6 +243,34 @@ def run_ours(args, rank, world, local_rank):
                      speedup_vsa_vs_dense=round(dms / ms, 2))
         del opd
 
+    # gate projection (the rest of vsa_forward/vsa_backward): tcgen05 GEMMs
+    # z = hidden.Wg (+bias, sigmoid, split) and dhidden / dWg / dbias, model_dim = H*d
+    gate = None
+    if cfg["B"] * cfg["H"] * cfg["d"] % 256 == 0 and (cfg["H"] * cfg["d"]) % 256 == 0:
+        md = cfg["H"] * cfg["d"]
+        hid = torch.randn((cfg["B"], 1, S, md), device=dev).to(dtype)
+        wg = (torch.randn((md, 2 * cfg["H"] * d), device=dev) / md ** 0.5).to(dtype)
+        gp = vsa.VsaParams(wg, torch.zeros(2 * cfg["H"] * d, device=dev), K, activation=1)
+        gcg, gfg = vsa.gates_from_hidden(hid, gp, cfg["H"], d, layout=L)
+        g0, g1, g2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        for _ in range(2):
+            vsa.gates_from_hidden(hid, gp, cfg["H"], d, layout=L)
+            vsa.gate_backward(hid, gp, gcg, gfg, q, k, layout=L)
+        g0.record(st)
+        for _ in range(5):
+            vsa.gates_from_hidden(hid, gp, cfg["H"], d, layout=L)
+        g1.record(st)
+        for _ in range(5):
+            vsa.gate_backward(hid, gp, gcg, gfg, q, k, layout=L)
+        g2.record(st)
+        torch.cuda.synchronize()
+        gfl = 2 * cfg["B"] * S * md * 2 * cfg["H"] * d
+        tf, tb = g0.elapsed_time(g1) / 5, g1.elapsed_time(g2) / 5
+        gate = {"model_dim": md, "fwd_ms": round(tf, 4), "fwd_tflops": round(gfl / tf / 1e9, 1),
+                "bwd_ms": round(tb, 4), "bwd_tflops": round(2 * gfl / tb / 1e9, 1),
+                "note": "not in value: the BASELINE metric is the attention op; gates are inputs there"}
+        del hid, wg, gcg, gfg
+
     # e2e through the public API with pinned host buffers: VsaHostPipeline overlaps the
     # H2D of unit-group i+1 and the D2H of group i-1 with the kernels of group i
     hin = [t.cpu().pin_memory() for t in (q, k, v, gc, gf, do)]
@@ -320,6 +348,7 @@ def run_ours(args, rank, world, local_rank):
                      "algorithmic_flops_per_launch": fl[dom]},
         "stages": stages,
         "dense_baseline": dense,
+        "gate_projection": gate,
         "e2e": {"value": round(world * fl["total"] / (ems * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                 "ms_per_step": round(ems, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
