@@ -360,13 +360,16 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int g0 = seq.next(2 * n);
         if (b) gq1 = g0; else gq0 = g0;
         const uint64_t q0 = dG0 + uint64_t((g0 * C::kGran) >> 4);
+        if (lane == 0) trace_ev(tr, 12, n);
         if (n >= 2) named_bar_b(kBarSdFree + b, kCompute + 32);
         named_bar_b(kBarGran, 64);
         tc_fence_after();
+        if (lane == 0) trace_ev(tr, 13, n);
 #pragma unroll
         for (int s = 0; s < D / 16; ++s)
           umma_bf16_warp(tbase + b * 64, q0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
                          dK0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+        if (lane == 0) trace_ev(tr, 14, n);
         umma_commit_warp(&sm->s_full[b]);
       };
       auto issue_dp = [&](int n) {
@@ -374,12 +377,15 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int g1 = seq.next(2 * n + 1);
         if (b) go1 = g1; else go0 = g1;
         const uint64_t o0 = dG0 + uint64_t((g1 * C::kGran) >> 4);
+        if (lane == 0) trace_ev(tr, 20, n);
         named_bar_b(kBarGran, 64);
         tc_fence_after();
+        if (lane == 0) trace_ev(tr, 21, n);
 #pragma unroll
         for (int s = 0; s < D / 16; ++s)
           umma_bf16_warp(tbase + 128 + b * 64, o0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
                          dV0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+        if (lane == 0) trace_ev(tr, 22, n);
         umma_commit_warp(&sm->dp_full[b]);
       };
       const uint64_t dP0 = make_sdesc_sw128(aP, 8192, 1024), dS0 = make_sdesc_sw128(aS, 8192, 1024);
@@ -397,11 +403,14 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           const int g = b ? go1 : go0;
           const uint32_t goff = uint32_t(g * C::kGran);
           const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
+          if (lane == 0) trace_ev(tr, 17, p);
           named_bar_b(kBarPFull, kCompute + 32);
           tc_fence_after();
+          if (lane == 0) trace_ev(tr, 18, p);
 #pragma unroll
           for (int s = 0; s < 8; ++s)
             umma_bf16_warp(tbase + 256, da + uint64_t(s * 128), dP0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+          if (lane == 0) trace_ev(tr, 19, p);
           umma_commit_warp(&sm->g_empty[g]);
         }
         if (p + 1 < npairs) issue_dp(p + 1);
@@ -409,11 +418,14 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           const int g = b ? gq1 : gq0;
           const uint32_t goff = uint32_t(g * C::kGran);
           const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
+          if (lane == 0) trace_ev(tr, 25, p);
           named_bar_b(kBarDsFull, kCompute + 32);
           tc_fence_after();
+          if (lane == 0) trace_ev(tr, 26, p);
 #pragma unroll
           for (int s = 0; s < 8; ++s)
             umma_bf16_warp(tbase + 320, da + uint64_t(s * 128), dS0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+          if (lane == 0) trace_ev(tr, 27, p);
           umma_commit_warp(&sm->g_empty[g]);
         }
       }

@@ -72,3 +72,19 @@ def test_invalid_arguments_are_rejected_without_a_gpu(lib):
     rc = lib.vsa_coarse_forward(C.byref(L), 1, 64, None, None, None, 0, None, None, None, None, None, None, None)
     assert rc < 0 and b"k must be in [1, num_cubes]" in lib.vsa_last_error()
     assert lib.vsa_fine_backward_workspace_bytes(C.byref(L), 2, 4) == 2 * 32 * 4 * (8192 + 4)
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    """bench.py --impl reference (the CPU reference arm: the oracle port) prints one
+    JSON line with the contract keys, on a tiny config."""
+    import json
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "tiny",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "impl", "cpu_baseline", "e2e", "higher_is_better"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "port"

@@ -1,5 +1,6 @@
 # SPDX-License-Identifier: Apache-2.0
-"""Debug: pipeline event trace of one dK/dV CTA on the Wan2.1-1.3B shape.
+"""Debug: pipeline event trace of one dK/dV CTA on the Wan2.1-1.3B shape. Needs the
+library built with trace probes: make -C paper_2505_13389_b200/csrc -B EXTRA=-DVSA_TRACE
 
 Uses vsa_debug_trace (fixed-slot clock64 stores, no atomics) and prints the events
 of the traced CTA in time order, relative to the first event."""
@@ -35,10 +36,9 @@ for cta in (300, 301):
     b = buf.cpu().tolist()
     ev = {(i // 256, i % 256): b[i] for i in range(cap) if b[i] != 0}
     t0 = ev.get((24, 0), min(ev.values()))
-    cols = [("ldQ", 2, lambda p: 2 * p), ("ldO", 2, lambda p: 2 * p + 1), ("dV0", 1, None),
-            ("gotS", 5, None), ("Prdy", 6, None), ("Pbuf", 8, None), ("gotdP", 9, None), ("dSrdy", 10, None),
-            ("dSbuf", 11, None), ("done", 7, None), ("xS", 16, None)]
-    print(f"=== dkdv cta {cta}: {len(ev)} events (cycles from first event; ld = TMA issue, S/dP/dV/dK = MMA issued)")
+    cols = [("S.w", 12, None), ("S.go", 13, None), ("S.end", 14, None), ("dV.w", 17, None), ("dV.go", 18, None),
+            ("dV.end", 19, None), ("dP.w", 20, None), ("dP.go", 21, None), ("dP.end", 22, None), ("dK.w", 25, None),
+            ("dK.go", 26, None), ("dK.end", 27, None), ("Prdy", 6, None), ("done", 7, None)]
     print("  p " + "".join(f"{n:>8s}" for n, _, _ in cols))
     names = {0: "entry", 4: "after TMEM alloc", 1: "epilogue start", 2: "epilogue rows written", 3: "exit"}
     print("  CTA:", {names[i]: ev[(24, i)] - t0 for i in names if (24, i) in ev}, "npairs ~", max([p for (c, p) in ev if c == 1] or [-1]) + 1)
