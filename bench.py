@@ -321,7 +321,7 @@ def run_ours(args, rank, world, local_rank):
             e["gbs"] = round(bytes_tp / (stage_ms[s] * 1e-3) / 1e9, 1)
         stages[s] = e
     line = {
-        "metric": "VSA fwd+bwd effective TFLOPS (algorithmic FLOPs / device time), Wan2.1-1.3B layer",
+        "metric": f"VSA fwd+bwd effective TFLOPS (algorithmic FLOPs / device time), {cfg['workload']}",
         "value": round(value, 2),
         "unit": "TFLOP/s",
         "n_gpus": world,

@@ -504,7 +504,11 @@ class VsaOp:
         flags = L.FINE_FORCE_SIMT if self.force_simt else 0
         wsb = lib.vsa_fine_backward_workspace_bytes(lr, bh, self.fine_k) if self.bwd_workspace else 0
         if wsb and (self.ws is None or self.ws.numel() < wsb):
-            self.ws = torch.empty(wsb, dtype=torch.uint8, device=dout.device)
+            free, _ = torch.cuda.mem_get_info(dout.device)
+            if wsb > 0.6 * free:  # e.g. the dense baseline at 14B (all cubes): dQ recomputes S / dP instead
+                wsb = 0
+            else:
+                self.ws = torch.empty(wsb, dtype=torch.uint8, device=dout.device)
         check(lib.vsa_fine_backward(lr, bh, d, dt, _p(qt), _p(kt), _p(vt), _p(self.dof), _p(self.lse),
                                     _p(self.delta), _p(self.fine_sel), self.fine_k, _p(self.selT_offs),
                                     _p(self.selT_idx), _p(self.dqc) if mean else None, _p(self.dkc) if mean else None,
