@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(128) prologue_kernel(DevLayout L, int64_t bh, 
       acc[i] = 0.f;
     }
   }
+#pragma unroll 4
   for (int o = 0; o < L.cube; ++o) {
     const int64_t pos = int64_t(c) * L.cube + o;
     const int64_t trow = u * L.seqp + pos;
@@ -65,11 +66,10 @@ __global__ void __launch_bounds__(128) prologue_kernel(DevLayout L, int64_t bh, 
         acc[i] = __fadd_rn(acc[i], __fmul_rn(g_o[i], g_c[i]));
       }
       store16(dof + trow * d + ch * V, r_f);
-      // delta uses the rounded dof actually fed to the fine backward
-      float r_fq[V];
-      load16(dof + trow * d + ch * V, r_fq);
+      // delta uses the rounded dof actually fed to the fine backward (the value store16
+      // wrote, re-rounded in registers: no dependent global round trip per token)
 #pragma unroll
-      for (int i = 0; i < V; ++i) part = __fmaf_rn(r_fq[i], f_o[i], part);
+      for (int i = 0; i < V; ++i) part = __fmaf_rn(to_f(from_f<T>(r_f[i])), f_o[i], part);
       if (dgc) {
         float t[V];
 #pragma unroll
