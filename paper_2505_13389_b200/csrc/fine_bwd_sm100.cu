@@ -654,22 +654,30 @@ __global__ void __launch_bounds__(kDQThreads, 2)
       }
     }
   } else if (warp == 5) {
-    if (lane == 0) {
-      const uint32_t idG = make_idesc_bf16(128, 64, true, false);  // A MN-major, B K-major
+    {  // whole warp issues (lean: descriptors by additions, one elected lane)
+      constexpr uint32_t idG = make_idesc_bf16(128, 64, true, false);  // A MN-major, B K-major
+      const uint32_t s0 = smem_u32(smem);
       for (int p = 0; p < npairs; ++p) {
         const int st = p % C::kStages;
         const bool hb = 2 * p + 1 < k_sel;
-        mbar_wait(&sm->full[st], (p / C::kStages) & 1);
-        tc_fence_after();
-        const uint32_t k0 = smem_u32(smem + st * C::kStage), d0 = k0 + C::kPair;
+        const uint32_t k0 = s0 + st * C::kStage, d0 = k0 + C::kPair;
         const uint32_t lbo = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - k0;
-        const int nsteps = hb ? 8 : 4;  // a single-cube last pair contributes 64 keys
-        for (int s = 0; s < nsteps; ++s)
-          umma_bf16(tbase, make_sdesc_sw128(k0 + s * 2048, lbo, 1024),
-                    make_sdesc_sw128(d0 + (s >> 2) * 8192 + (s & 3) * 32, 16, 1024), idG, (p > 0 || s > 0) ? 1u : 0u);
-        umma_commit(&sm->empty[st]);
+        const uint64_t ad = make_sdesc_sw128(k0, lbo, 1024), bd = make_sdesc_sw128(d0, 16, 1024);
+        mbar_wait_warp(&sm->full[st], (p / C::kStages) & 1);
+        tc_fence_after();
+        if (hb) {
+#pragma unroll
+          for (int s = 0; s < 8; ++s)
+            umma_bf16_warp(tbase, ad + uint64_t(s * 128), bd + uint64_t(((s >> 2) * 8192 + (s & 3) * 32) >> 4), idG,
+                           (p > 0 || s > 0) ? 1u : 0u);
+        } else {  // a single-cube last pair contributes 64 keys
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            umma_bf16_warp(tbase, ad + uint64_t(s * 128), bd + uint64_t((s * 32) >> 4), idG, (p > 0 || s > 0) ? 1u : 0u);
+        }
+        umma_commit_warp(&sm->empty[st]);
       }
-      umma_commit(&sm->final_bar);
+      umma_commit_warp(&sm->final_bar);
     }
   } else if (warp < 4) {
     const int dl = warp * 32 + lane;
