@@ -85,7 +85,7 @@ struct FwdSmall {
 
 // named barrier IDs (bar 0 = __syncthreads)
 constexpr int kFbSoft = 1 /* 1,2: one per column half */, kFbPFull = 3 /* 3,4 */, kFbSFree = 5 /* 5,6 */,
-              kFbOFree = 7 /* 7,8 */, kFbGran = 9, kFbAll = 10 /* both softmax halves */,
+              kFbOFree = 7 /* 7,8 */, kFbGran = 9,
               kFbLReady = 11 /* 11,12 */, kFbEpDone = 13 /* 13,14 */, kFbEpi = 15 /* epilogue warps */;
 // register budgets (setmaxnreg): softmax warpgroups / epilogue warpgroup / producer-MMA-watcher
 constexpr int kRegSoft = 184, kRegEpi = 88, kRegCtl = 56;  // 256*184 + 128*88 + 128*56 = 65536
@@ -361,10 +361,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // per-lane (key) partial row sums of the 32 queries of this half, in registers
     float lsum[32];
     for (int j = 0; j < ntask_local; ++j) {
-      const int t = int(blockIdx.x) + j * ncta;
-      const int64_t u = t / L.nc;
-      const int qc = t - int(u) * L.nc;
-      const int row0 = int(u * L.seqp);
       const int tb = j & 1;
       const uint32_t tO = lrow + 128 + tb * 64 + qb0;
 #pragma unroll
