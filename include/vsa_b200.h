@@ -214,6 +214,21 @@ int vsa_gate_backward(const vsa_layout_t* layout, int64_t batch, int64_t heads, 
                       float* dweight, float* dbias, void* stream);
 size_t vsa_gate_backward_workspace_bytes(const vsa_layout_t* layout, int64_t batch, int64_t heads, int64_t d);
 
+/* Selection analytics (analysis.hpp:100-147, dense.hpp:214-240).
+ * vsa_selection_accuracy_from_lse: acc[u] = mean_i exp(lse_sel[u,i] - lse_all[u,i]) (double),
+ * the attention mass captured by a block map, from the row log-sum-exps of vsa_fine_forward
+ * run with the selection and with all cubes — equal to selection_accuracy(
+ * aggregate_probs_to_cubes(dense_probs(q, k)), sel) without any [S,S] matrix.
+ * vsa_aggregate_probs_to_cubes / vsa_selection_accuracy: the reference's diagnostics on
+ * materialised fp32 probabilities ([bh,S,S] -> [bh,S,nc]; [bh,S,nc] + sel -> acc), unpadded
+ * layouts. */
+int vsa_selection_accuracy_from_lse(const float* lse_sel, const float* lse_all, int64_t bh, int64_t seq,
+                                    double* acc, void* stream);
+int vsa_aggregate_probs_to_cubes(const vsa_layout_t* layout, int64_t bh, const float* probs, float* out,
+                                 void* stream);
+int vsa_selection_accuracy(const vsa_layout_t* layout, int64_t bh, const float* probs_cube, const int32_t* sel,
+                           int64_t top_k, double* acc, void* stream);
+
 /* Ulysses resharding copy: dst[i1][i0] = src[i0][i1] over an
  * [n0][n1] grid of contiguous blocks of `block_bytes` (a multiple of 16). With
  * n0 = B*S/P, n1 = P, block = (H/P)*d*elem it packs a sequence shard [B,S/P,H,d]

@@ -594,3 +594,41 @@ def max_rel_err(a, f) -> float:
     f = np.asarray(f, np.float64).reshape(-1)
     den = np.maximum(np.maximum(np.abs(a), np.abs(f)), 1.0)
     return float(np.max(np.abs(a - f) / den)) if a.size else 0.0
+
+
+# ----------------------------------------------------------------------------- selection analytics
+def dense_probs(q, k):
+    """dense_probs (dense.hpp:214-240): row-stochastic [B,H,S,S] attention probabilities
+    (no mask), max-subtracted exp / row sum, float64 here."""
+    q = np.asarray(q, np.float64)
+    k = np.asarray(k, np.float64)
+    d = q.shape[-1]
+    s = np.einsum("bhid,bhjd->bhij", q, k) * (1.0 / np.sqrt(d))
+    s = np.exp(s - s.max(axis=-1, keepdims=True))
+    return s / s.sum(axis=-1, keepdims=True)
+
+
+def aggregate_probs_to_cubes(layout, probs_token):
+    """aggregate_probs_to_cubes (analysis.hpp:130-147): [..,S,S] tile-ordered -> [..,S,nc]."""
+    B, H, S, S2 = probs_token.shape
+    if S != layout.seq_len or S2 != layout.seq_len:
+        raise ValueError("aggregate_probs_to_cubes: expected [.., seq, seq] probabilities")
+    return probs_token.reshape(B, H, S, layout.num_cubes, layout.cube_size).sum(axis=-1)
+
+
+def selection_accuracy(layout, probs_cube, sel):
+    """selection_accuracy (analysis.hpp:100-125): captured attention mass of the selected
+    cubes, averaged over query tokens, per (b, h) -> float64 [B, H]."""
+    B, H, S, nc = probs_cube.shape
+    if S != layout.seq_len or nc != layout.num_cubes:
+        raise ValueError("selection_accuracy: probabilities do not match layout")
+    if sel.shape[:3] != (B, H, nc):
+        raise ValueError("selection_accuracy: selection does not match shapes")
+    cube = layout.cube_size
+    qcube = np.arange(S) // cube
+    acc = np.empty((B, H), np.float64)
+    for b in range(B):
+        for h in range(H):
+            rows = sel[b, h][qcube]  # [S, K] selected cubes of each token's query cube
+            acc[b, h] = np.take_along_axis(probs_cube[b, h].astype(np.float64), rows, axis=1).sum() / S
+    return acc

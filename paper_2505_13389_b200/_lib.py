@@ -35,6 +35,7 @@ EXPORTS = [
     "vsa_validate_selection", "vsa_fine_forward", "vsa_backward_prologue", "vsa_coarse_backward",
     "vsa_fine_backward", "vsa_fine_backward_workspace_bytes", "vsa_unpool_max_add", "vsa_layout_set_io",
     "vsa_transpose_blocks", "vsa_gate_forward", "vsa_gate_backward", "vsa_gate_backward_workspace_bytes",
+    "vsa_selection_accuracy_from_lse", "vsa_aggregate_probs_to_cubes", "vsa_selection_accuracy",
 ]
 
 
@@ -74,6 +75,9 @@ def lib():
         "vsa_gate_forward": [LP, I64, I64, I64, I64, P, P, P, I32, I32, P, P, P],
         "vsa_gate_backward": [LP, I64, I64, I64, I64, P, P, P, P, P, P, I32, I32, P, P, P, P, P],
         "vsa_gate_backward_workspace_bytes": [LP, I64, I64, I64],
+        "vsa_selection_accuracy_from_lse": [P, P, I64, I64, P, P],
+        "vsa_aggregate_probs_to_cubes": [LP, I64, P, P, P],
+        "vsa_selection_accuracy": [LP, I64, P, P, I64, P, P],
         "vsa_flatten_index": [LP, I64, I64, I64, C.POINTER(I64)],
         "vsa_tile": [LP, I64, I64, I32, P, P, P],
         "vsa_untile": [LP, I64, I64, I32, P, P, P],

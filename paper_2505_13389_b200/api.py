@@ -680,3 +680,45 @@ def gate_backward(hidden, params: VsaParams, gc, gf, dgc, dgf, layout=None, op=N
                                 1 if params.adaptation else 0, _p(ws), _p(dhidden), _p(dW),
                                 _p(db) if db is not None else None, _stream()))
     return dhidden, dW, db
+
+
+# ----------------------------------------------------------------------------- selection analytics (§8 f4)
+def aggregate_probs_to_cubes(layout: TileLayout, probs: torch.Tensor) -> torch.Tensor:
+    """aggregate_probs_to_cubes (analysis.hpp:130-147): fp32 [B,H,S,S] tile-ordered token
+    probabilities -> [B,H,S,nc] (unpadded layouts, diagnostics at small S)."""
+    _cuda4(probs, "probs")
+    B, H, S, S2 = probs.shape
+    if S != layout.seq_len or S2 != layout.seq_len or probs.dtype != torch.float32:
+        raise ValueError("aggregate_probs_to_cubes: expected fp32 [.., seq, seq] probabilities")
+    out = torch.empty((B, H, S, layout.num_cubes), dtype=torch.float32, device=probs.device)
+    check(L.lib().vsa_aggregate_probs_to_cubes(layout.ref(), B * H, _p(probs), _p(out), _stream()))
+    return out
+
+
+def selection_accuracy(layout: TileLayout, probs_cube: torch.Tensor, sel: torch.Tensor) -> torch.Tensor:
+    """selection_accuracy (analysis.hpp:100-125): mean captured mass per (b, h), float64 [B,H]."""
+    _cuda4(probs_cube, "probs_cube")
+    B, H, S, nc = probs_cube.shape
+    if S != layout.seq_len or nc != layout.num_cubes or probs_cube.dtype != torch.float32:
+        raise ValueError("selection_accuracy: probabilities do not match layout")
+    if tuple(sel.shape[:3]) != (B, H, nc):
+        raise ValueError("selection_accuracy: selection does not match shapes")
+    acc = torch.empty((B, H), dtype=torch.float64, device=probs_cube.device)
+    check(L.lib().vsa_selection_accuracy(layout.ref(), B * H, _p(probs_cube), _p(sel), sel.shape[3], _p(acc),
+                                         _stream()))
+    return acc
+
+
+def selection_accuracy_qk(layout: TileLayout, q: torch.Tensor, k: torch.Tensor, sel: torch.Tensor) -> torch.Tensor:
+    """Captured dense-attention mass of a block map straight from Q, K (tile-ordered):
+    mean_i exp(lse_sel(i) - lse_all(i)) from two fine forwards (the selection and all
+    cubes) — the same quantity as selection_accuracy(aggregate_probs_to_cubes(
+    dense_probs(q, k)), sel) without the [S,S] matrix. float64 [B,H]."""
+    if layout.seq_padded != layout.seq_len:
+        raise ValueError("selection_accuracy_qk: padded layouts are not supported")
+    B, H, S, d = q.shape
+    lse_sel = fine_forward(layout, q, k, k, sel).row_lse
+    lse_all = fine_forward(layout, q, k, k, all_cubes(B, H, layout.num_cubes, device=q.device)).row_lse
+    acc = torch.empty((B, H), dtype=torch.float64, device=q.device)
+    check(L.lib().vsa_selection_accuracy_from_lse(_p(lse_sel), _p(lse_all), B * H, S, _p(acc), _stream()))
+    return acc
