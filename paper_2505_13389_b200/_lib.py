@@ -12,7 +12,7 @@ import os
 import subprocess
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libvsa_b200.so")
+LIB_PATH = os.environ.get("VSA_LIB_PATH") or os.path.join(_PKG, "_lib", "libvsa_b200.so")  # override: A/B tools
 CSRC = os.path.join(_PKG, "csrc")
 
 VSA_F32, VSA_BF16 = 0, 1

@@ -578,6 +578,10 @@ __global__ void __launch_bounds__(kKVThreads, 1)
 //   [64 q][64 keys] tiles, K-major, one 64-key chunk per tile of the pair.
 // 2 CTAs/SM (one epilogue overlaps the other's stream), 2-stage {Kpair, dS pair} ring.
 constexpr int kDQThreads = 192;
+#ifndef VSA_DQ_PREFETCH
+#define VSA_DQ_PREFETCH 8
+#endif
+constexpr int kDQPrefetch = VSA_DQ_PREFETCH;  // dS tiles prefetched into L2 ahead (0 = off)
 
 template <int D>
 struct DQCfg {
@@ -634,8 +638,15 @@ __global__ void __launch_bounds__(kDQThreads, 2)
     if (lane == 0) {
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_ds);
+      // The dS stream comes from HBM (the K pairs hit L2): keep kDQPrefetch tiles in
+      // flight into L2 ahead of the 2-stage SMEM ring (measured: ~0.05 ms per step).
+      const int pf0 = min(kDQPrefetch, k_sel);
+      for (int t = 0; t < pf0; ++t) tma_prefetch_l2_2d(&tm_ds, 0, int(ds_row0 + int64_t(t) * 64));
       for (int p = 0; p < npairs; ++p) {
         const int st = p % C::kStages;
+        if (kDQPrefetch > 0)
+          for (int t = 2 * p + kDQPrefetch; t < min(2 * p + 2 + kDQPrefetch, k_sel); ++t)
+            tma_prefetch_l2_2d(&tm_ds, 0, int(ds_row0 + int64_t(t) * 64));
         const bool hb = 2 * p + 1 < k_sel;
         uint8_t* sK = smem + st * C::kStage;
         uint8_t* sD = sK + C::kPair;

@@ -33,5 +33,5 @@ for p in range(0, 120):
     row = [ev.get((code, f(p) if f else p)) for _, code, f in cols]
     if all(r is None for r in row):
         break
-    if 8 <= p < 12:
+    if 8 <= p < 24:
         print(f"{p:4d}" + "".join(f"{(r - t0) if r else -1:8d}" for r in row))
