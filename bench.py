@@ -546,7 +546,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=4, help="host-pipeline unit groups for the e2e leg")
+    ap.add_argument("--e2e-chunks", type=int, default=12, help="host-pipeline unit groups for the e2e leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -538,7 +538,7 @@ class VsaHostPipeline:
     inputs/outputs, events for the hand-offs. Result == VsaOp on the whole batch.
     """
 
-    def __init__(self, layout: TileLayout, B: int, H: int, d: int, top_k: int, chunks: int = 4,
+    def __init__(self, layout: TileLayout, B: int, H: int, d: int, top_k: int, chunks: int = 12,
                  dtype=torch.bfloat16, device="cuda", **op_kwargs):
         units = B * H
         chunks = max(1, min(chunks, units))
@@ -554,43 +554,61 @@ class VsaHostPipeline:
         self.d2h_bytes = self.h2d_bytes
 
     def run(self, hin, hout):
-        """hin = (q, k, v, gc, gf, dO), hout = (O, dQ, dK, dV, dGc, dGf): pinned host [B,H,S,d]."""
+        """hin = (q, k, v, gc, gf, dO), hout = (O, dQ, dK, dV, dGc, dGf): pinned host [B,H,S,d].
+
+        Per group: the five forward inputs are copied first and the forward starts as
+        soon as they land (dO follows on the copy stream); O is copied out while the
+        backward runs, the five gradients after it."""
         flat = lambda t: t.view(self.units, self.S, self.d)
         hin, hout = [flat(t) for t in hin], [flat(t) for t in hout]
         comp = torch.cuda.current_stream()
         n = len(self.bounds) - 1
-        ev_in, ev_comp, ev_out = [None] * n, [None] * n, [None] * n
+        ev_comp, ev_out = [None] * n, [None] * n
+        ev = lambda: torch.cuda.Event()
         for i in range(n):
             a, b = self.bounds[i], self.bounds[i + 1]
             c, slot = b - a, i % 2
+            di, do = self.din[slot], self.dout[slot]
             with torch.cuda.stream(self.s_in):
                 if i >= 2:
                     self.s_in.wait_event(ev_comp[i - 2])      # slot's inputs consumed
-                for dst, src in zip(self.din[slot], hin):
+                for dst, src in zip(di[:5], hin[:5]):
                     dst[0, :c].copy_(src[a:b], non_blocking=True)
-                ev_in[i] = torch.cuda.Event()
-                ev_in[i].record(self.s_in)
-            comp.wait_event(ev_in[i])
+                ev_fwd_in = ev()
+                ev_fwd_in.record(self.s_in)
+                di[5][0, :c].copy_(hin[5][a:b], non_blocking=True)
+                ev_bwd_in = ev()
+                ev_bwd_in.record(self.s_in)
+            comp.wait_event(ev_fwd_in)
             if i >= 2:
                 comp.wait_event(ev_out[i - 2])                # slot's outputs drained
-            op, di, do = self.ops[slot], self.din[slot], self.dout[slot]
+            op = self.ops[slot]
             if c == op.H:
                 op.forward(*di[:5], out=do[0], check_inputs=False)
+                ev_fwd = ev()
+                ev_fwd.record(comp)
+                with torch.cuda.stream(self.s_out):
+                    self.s_out.wait_event(ev_fwd)
+                    hout[0][a:b].copy_(do[0][0, :c], non_blocking=True)
+                comp.wait_event(ev_bwd_in)
                 op.backward(di[5], *do[1:], check_inputs=False)
+                first_out = 1
             else:  # ragged last group: run on views of the right head count
+                comp.wait_event(ev_bwd_in)
                 sub = VsaOp(op.layout, 1, c, self.d, op.top_k, dtype=self.dtype, device=di[0].device)
                 v = lambda t: t[:, :c].contiguous()
                 o = sub.forward(*(v(t) for t in di[:5]))
                 g = sub.backward(v(di[5]))
                 for dst, src in zip(do, (o, *g)):
                     dst[:, :c].copy_(src)
-            ev_comp[i] = torch.cuda.Event()
+                first_out = 0
+            ev_comp[i] = ev()
             ev_comp[i].record(comp)
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(ev_comp[i])
-                for dst, src in zip(hout, do):
+                for dst, src in zip(hout[first_out:], do[first_out:]):
                     dst[a:b].copy_(src[0, :c], non_blocking=True)
-                ev_out[i] = torch.cuda.Event()
+                ev_out[i] = ev()
                 ev_out[i].record(self.s_out)
         comp.wait_event(ev_out[n - 1])
         if n >= 2:
