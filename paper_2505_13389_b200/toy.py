@@ -124,6 +124,58 @@ class SparsitySchedule:
         return max(self.k_target, self.k_start - self.decrement * drops)
 
 
+SPATIAL_TEMPORAL, STRIDED_WINDOW, COMPRESS_KV = 0, 1, 2
+SPATIAL, TEMPORAL = 0, 1
+
+
+@dataclass
+class PatternSpec:
+    """PatternSpec (analysis.hpp:78-86): the fixed-pattern baselines."""
+
+    kind: int = SPATIAL_TEMPORAL
+    phase: int = SPATIAL
+    window_s: int = 8
+    window_t: int = 2
+
+
+def fixed_pattern_selection(layout: TileLayout, spec: PatternSpec) -> np.ndarray:
+    """fixed_pattern_selection (analysis.cpp:99-157): the pattern's connectivity at cube
+    granularity, [num_cubes, row_len] int32 ascending. Windows must be cube-aligned so
+    every row selects the same number of cubes; raises ValueError otherwise."""
+    L = layout
+    if spec.kind == STRIDED_WINDOW:
+        if spec.window_t < 1 or spec.window_s < 1:
+            raise ValueError("fixed pattern: window sizes must be >= 1")
+        if spec.phase == SPATIAL:
+            if spec.window_t % L.cube_t or L.tokens_t % spec.window_t:
+                raise ValueError("fixed pattern: temporal window must be cube-aligned")
+        elif (spec.window_s % L.cube_h or spec.window_s % L.cube_w or L.tokens_h % spec.window_s
+              or L.tokens_w % spec.window_s):
+            raise ValueError("fixed pattern: spatial window must be cube-aligned")
+    c = np.arange(L.num_cubes)
+    ct, ch, cw = c // (L.cubes_h * L.cubes_w), (c // L.cubes_w) % L.cubes_h, c % L.cubes_w
+    t, h, w = ct * L.cube_t, ch * L.cube_h, cw * L.cube_w  # cube representatives
+    if spec.kind == SPATIAL_TEMPORAL:
+        allow = (ct[:, None] == ct[None, :]) if spec.phase == SPATIAL else \
+            (ch[:, None] == ch[None, :]) & (cw[:, None] == cw[None, :])
+    elif spec.kind == STRIDED_WINDOW:
+        if spec.phase == SPATIAL:
+            allow = (t[:, None] // spec.window_t) == (t[None, :] // spec.window_t)
+        else:
+            ws = spec.window_s
+            allow = ((h[:, None] // ws) == (h[None, :] // ws)) & ((w[:, None] // ws) == (w[None, :] // ws))
+    elif spec.kind == COMPRESS_KV:
+        allow = np.ones((L.num_cubes, L.num_cubes), dtype=bool)
+    else:
+        raise ValueError("fixed pattern: unknown kind")
+    counts = allow.sum(axis=1)
+    if (counts != counts[0]).any():
+        raise ValueError("fixed pattern: window sizes give uneven selection rows")
+    if counts[0] < 1:
+        raise ValueError("fixed pattern: empty selection row")
+    return np.nonzero(allow)[1].reshape(L.num_cubes, int(counts[0])).astype(np.int32)
+
+
 @dataclass
 class OptimizerSettings:
     kind: str = "adam"  # "adam" | "sgd"
@@ -135,7 +187,7 @@ class OptimizerSettings:
 
 @dataclass
 class ToyTrainConfig:
-    """ToyTrainConfig (toy.hpp:120-131); policy "learned" | "fixed_random"."""
+    """ToyTrainConfig (toy.hpp:120-131); policy "learned" | "fixed_random" | "fixed_pattern"."""
 
     batch_size: int = 4
     steps: int = 5000
@@ -145,6 +197,7 @@ class ToyTrainConfig:
     schedule: Optional[SparsitySchedule] = None
     optimizer: OptimizerSettings = field(default_factory=OptimizerSettings)
     policy: str = "learned"
+    pattern: PatternSpec = field(default_factory=PatternSpec)  # used by "fixed_pattern"
     seed: int = 1
 
 
@@ -215,8 +268,16 @@ def train_toy(task: PlantedTask, cfg: ToyTrainConfig, device="cuda", dtype=torch
         fixed_sel = torch.from_numpy(np.stack([np.sort(sg.choice(L.num_cubes, cfg.top_k, replace=False))
                                                for _ in range(B * H * L.num_cubes)]).astype(np.int32)
                                      ).reshape(B, H, L.num_cubes, cfg.top_k).to(device)
-    elif cfg.policy != "learned":
-        raise ValueError("train_toy: policy must be 'learned' or 'fixed_random'")
+    elif cfg.policy not in ("learned", "fixed_pattern"):
+        raise ValueError("train_toy: policy must be 'learned', 'fixed_random' or 'fixed_pattern'")
+    pattern_sel = {}
+    if cfg.policy == "fixed_pattern":
+        # spatial-temporal controls alternate phases across steps (toy.hpp:276-285)
+        phases = (SPATIAL, TEMPORAL) if cfg.pattern.kind == SPATIAL_TEMPORAL else (cfg.pattern.phase,)
+        for ph in phases:
+            rows = fixed_pattern_selection(L, PatternSpec(cfg.pattern.kind, ph, cfg.pattern.window_s,
+                                                          cfg.pattern.window_t))
+            pattern_sel[ph] = torch.from_numpy(rows).to(device).expand(cfg.batch_size, H, *rows.shape).contiguous()
     adam = {n: (torch.zeros_like(w), torch.zeros_like(w)) for n, w in model.items()}
     ops = {}
     hid = data.hidden[:, 0]  # [B, S, md]
@@ -232,15 +293,20 @@ def train_toy(task: PlantedTask, cfg: ToyTrainConfig, device="cuda", dtype=torch
     for step in range(cfg.steps):
         k_step = cfg.schedule.k_at(step) if cfg.schedule is not None else cfg.top_k
         k_step = min(max(k_step, 1), L.num_cubes)
-        if k_step not in ops:
-            ops[k_step] = VsaOp(L, B, H, d, k_step, dtype=dtype, pool=cfg.pool, raster=False, device=device)
-        op = ops[k_step]
+        sel_override = fixed_sel
+        if cfg.policy == "fixed_pattern":
+            sel_override = pattern_sel[(SPATIAL, TEMPORAL)[step % 2]] if len(pattern_sel) == 2 \
+                else next(iter(pattern_sel.values()))
+        k_op = k_step if sel_override is None else sel_override.shape[-1]
+        if k_op not in ops:
+            ops[k_op] = VsaOp(L, B, H, d, k_op, dtype=dtype, pool=cfg.pool, raster=False, device=device)
+        op = ops[k_op]
         q, k, v = (heads(hid @ model[w]) for w in ("wq", "wk", "wv"))
         z = hid @ model["gate_weight"]
         if cfg.activation == 1:
             z = torch.sigmoid(z)
         gc, gf = heads(z[..., :pc]), heads(z[..., pc:])
-        out = op.forward(q, k, v, gc, gf, sel_override=fixed_sel)
+        out = op.forward(q, k, v, gc, gf, sel_override=sel_override)
         dout = out - data.target
         loss = float((dout.double() ** 2).sum()) / n
         recall = planted_recall(op.fine_sel, data.planted)
@@ -268,6 +334,7 @@ def train_toy(task: PlantedTask, cfg: ToyTrainConfig, device="cuda", dtype=torch
             w -= opt.lr * (m / bc1) / ((vv / bc2).sqrt() + opt.eps)
     h = 0xCBF29CE484222325
     for name in ("wq", "wk", "wv", "gate_weight"):
-        h = _fnv1a64(model[name].detach().cpu().numpy().tobytes(), h)
+        # column-major bytes, as the reference hashes its Eigen matrices
+        h = _fnv1a64(model[name].detach().t().contiguous().cpu().numpy().tobytes(), h)
     rep.snapshot_id = f"{h:016x}"
     return rep

@@ -91,3 +91,28 @@ def test_learned_selection_beats_fixed_random(vsa):
     assert not learned.diverged and not fixed.diverged
     assert learned.final_recall() > fixed.final_recall()
     assert learned.final_loss() < fixed.final_loss()
+
+
+def test_acceptance_7_default_task(vsa):
+    """SPEC acceptance 7: the default planted-cube task (vsa_cli.cpp:515-523
+    train-toy defaults) reaches recall >= 0.8 and final MSE <= 1.10x the dense control's
+    within 5000 steps, and the learned selection beats the fixed-random control."""
+    from paper_2505_13389_b200.toy import PlantedTask, ToyTrainConfig, train_toy
+
+    task = PlantedTask(vsa.TileLayout(8, 8, 8, 2, 2, 2), planted_count=4, heads=2, head_dim=8, seed=0)
+    run = lambda k, policy: train_toy(task, ToyTrainConfig(batch_size=4, steps=5000, top_k=k, policy=policy, seed=1))
+    learned, dense, fixed = run(8, "learned"), run(task.layout.num_cubes, "learned"), run(8, "fixed_random")
+    assert not (learned.diverged or dense.diverged or fixed.diverged)
+    assert learned.final_recall() >= 0.8
+    assert learned.final_loss() <= 1.10 * dense.final_loss()
+    assert learned.final_recall() > fixed.final_recall()
+
+
+def test_fixed_pattern_control_runs(vsa):
+    from paper_2505_13389_b200.toy import PatternSpec, ToyTrainConfig, train_toy
+
+    task = small_task(vsa)
+    rep = train_toy(task, ToyTrainConfig(batch_size=2, steps=6, top_k=2, policy="fixed_pattern",
+                                         pattern=PatternSpec()))  # spatial-temporal, alternating phases
+    assert len(rep.steps) == 6 and not rep.diverged
+    assert all(0.0 <= s.recall <= 1.0 for s in rep.steps)
