@@ -51,3 +51,21 @@ def test_selection_accuracy_matches_oracle(vsa, dtype):
     full = vsa.all_cubes(B, H, L.num_cubes)
     np.testing.assert_allclose(vsa.selection_accuracy_qk(L, dev(qt, dtype), dev(kt, dtype), full).cpu().numpy(), 1.0,
                                rtol=1e-6)
+
+
+def test_acceptance_6_selection_metric_sanity(vsa):
+    """SPEC acceptance 6 / test_analysis.cpp:68-99 on the GPU kernels: uniform attention
+    captures exactly K/num_cubes; random selections average K/num_cubes within 0.01."""
+    L = vsa.TileLayout(8, 8, 8, 2, 2, 2)  # 512 tokens, 64 cubes
+    nc, k = L.num_cubes, 8
+    uniform = torch.full((1, 1, L.seq_len, nc), 1.0 / nc, device="cuda")
+    full = vsa.all_cubes(1, 1, nc)
+    assert vsa.selection_accuracy(L, uniform, full).item() == 1.0
+    gen = np.random.default_rng(91)
+    rsel = lambda: torch.from_numpy(np.sort(np.stack([gen.choice(nc, k, replace=False) for _ in range(nc)]), axis=1)
+                                    .astype(np.int32)).view(1, 1, nc, k).cuda()
+    assert vsa.selection_accuracy(L, uniform, rsel()).item() == k / nc
+    rows = torch.from_numpy(gen.standard_normal((L.seq_len, nc))).cuda()
+    probs = torch.softmax(rows, dim=1).float().view(1, 1, L.seq_len, nc).contiguous()
+    mean = sum(vsa.selection_accuracy(L, probs, rsel()).item() for _ in range(100)) / 100
+    assert abs(mean - k / nc) < 0.01

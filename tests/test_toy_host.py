@@ -51,3 +51,22 @@ def test_strided_window_covering_grid_is_full():
     assert full.shape == (L.num_cubes, L.num_cubes)
     w2 = fixed_pattern_selection(L, PatternSpec(STRIDED_WINDOW, SPATIAL, 8, 2))
     assert w2.shape == (L.num_cubes, L.cubes_h * L.cubes_w)  # window_t = cube_t: one cube layer per window
+
+
+def test_flop_accounting_exact_8x():
+    """test_analysis.cpp:43-66 / SPEC acceptance 4."""
+    from paper_2505_13389_b200.analysis import FULL, VSA, FlopsConfig, compute_flops, sparsity_density
+
+    cfg = FlopsConfig(n_params=1e6, n_tokens=1e3, seq_len=16384, n_heads=12, head_dim=64, n_layers=12,
+                      block_size=64, density=sparsity_density(32, 64, 16384))
+    assert cfg.density == 0.125
+    full, sparse = compute_flops(cfg, FULL), compute_flops(cfg, VSA)
+    assert full.model_flops == 6e9 and sparse.model_flops == 6e9
+    assert full.attention_flops / sparse.attention_flops == 8.0
+    assert sparse.attention_flops / full.attention_flops == cfg.density
+    assert sparse.coarse_flops == full.attention_flops / (64.0 * 64.0)
+    assert sparse.total == sparse.model_flops + sparse.attention_flops + sparse.coarse_flops
+    js = sparse.to_json()
+    assert '"model_flops"' in js and '"density": 0.125' in js
+    with pytest.raises(ValueError):
+        compute_flops(FlopsConfig(), VSA)
