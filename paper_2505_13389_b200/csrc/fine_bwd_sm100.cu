@@ -25,7 +25,17 @@
 // TMA producers, warp 10 TMEM allocator + single-thread MMA issuer. S / dP are
 // double-buffered in TMEM by pair parity, operand stages and P / dS smem buffers
 // likewise, and the MMA issuer runs one pair ahead: the exp2 / dS math of pairs
-// p and p+1 overlaps the products of p-1, p+1 and p+2.
+// p and p+1 overlaps the products of p-1, p+1 and p+2. (That describes the
+// recompute dQ fallback, K6b without a workspace.)
+//
+// K6c dK/dV is persistent (one CTA per SM, 512 threads): tasks (unit, key cube) are
+// claimed from a global counter and published through an SMEM ring; warps 0-7 compute
+// P / dS, 8 streams the Q / dO granules (the ring runs on across tasks), 9 stores dS
+// tiles (lane 0) and loads each task's K / V (lane 1), 10 issues the MMAs, 11 watches
+// the loads, 12-15 run the epilogue of task j (dK^T / dV^T from a TMEM buffer double-
+// buffered by task parity) while task j+1 computes. Per-CTA launch, TMEM allocation
+// and epilogue costs (~9000 cycles per key cube) are gone; the dynamic hand-out keeps
+// the very uneven list lengths of the transposed map balanced.
 #include <cmath>
 
 #include "common.cuh"
@@ -36,7 +46,10 @@
 namespace vsa_dev {
 
 constexpr int kBwdThreads = 352;
-constexpr int kKVThreads = 384;  // dK/dV: + a load-watcher warp
+constexpr int kKVThreads = 512;  // dK/dV (persistent): + load watcher, + 4 epilogue warps
+constexpr int kEpiThreads = 128;
+// register budgets (setmaxnreg): compute / epilogue / producer-store-issuer-watcher warps
+constexpr int kKVRegCmp = 160, kKVRegEpi = 96, kKVRegCtl = 72;
 constexpr int kCompute = 256;  // two warpgroups
 
 __device__ __forceinline__ float ex2b(float x) {
@@ -190,13 +203,20 @@ struct KVCfg {
   static_assert(kTiles <= 225 * 1024, "dK/dV smem budget");
 };
 
+constexpr int kTaskRing = 8;
+// task counter of launches without a workspace (the dS fallback path)
+__device__ int g_dkdv_task_ctr;
+// task-ring readers: dS-store thread, watcher, issuer, 8 compute warps, 4 epilogue warps
+constexpr int kTaskConsumers = 1 + 1 + 1 + 8 + 4;
+
 struct KVSmall {
-  alignas(16) float xk[128], xv[128];  // cube-level unpool rows dKc, dVc of this key cube
-  int64_t rows[64];                      // output row of each token of the key cube
-  uint64_t kv_full, final_bar;
+  uint64_t kv_full, kv_empty;
+  uint64_t task_full[kTaskRing], task_empty[kTaskRing];
+  int task_id[kTaskRing];
   uint64_t g_full[10], g_empty[10];
-  uint64_t s_full[2], dp_full[2], sd_free[2];
-  uint64_t p_full[2], ds_full[2], ds_stored[2];
+  uint64_t s_full[2], dp_full[2];
+  uint64_t acc_full[2], acc_free[2];  // dK / dV accumulators by task parity
+  uint64_t ds_full[2], ds_stored[2];
   uint32_t tmem;
 };
 
@@ -204,12 +224,13 @@ template <int D>
 __global__ void __launch_bounds__(kKVThreads, 1)
     fine_dkdv_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                           DevLayout L, int k_sel, float scale, float scale_log2, const float* __restrict__ lse,
-                           const float* __restrict__ delta, const int32_t* __restrict__ offs,
-                           const int32_t* __restrict__ idx, const float* __restrict__ dkc,
-                           const float* __restrict__ dvc, int raster, __nv_bfloat16* __restrict__ dk,
-                           __nv_bfloat16* __restrict__ dv, const __grid_constant__ CUtensorMap tm_ds,
-                           const int32_t* __restrict__ ds_pos, int ds_store, TraceCfg tr) {
+                           DevLayout L, int ntasks, int k_sel, float scale, float scale_log2,
+                           const float* __restrict__ lse, const float* __restrict__ delta,
+                           const int32_t* __restrict__ offs, const int32_t* __restrict__ idx,
+                           const float* __restrict__ dkc, const float* __restrict__ dvc, int raster,
+                           __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv,
+                           const __grid_constant__ CUtensorMap tm_ds, const int32_t* __restrict__ ds_pos, int ds_store,
+                           int* __restrict__ task_ctr, TraceCfg tr) {
   using C = KVCfg<D>;
   constexpr int NG = C::kNG, NPB = C::kNPB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -224,19 +245,36 @@ __global__ void __launch_bounds__(kKVThreads, 1)
 
   if (threadIdx.x == 0) trace_ev(tr, 24, 0);
   const int warp = int(warp_id()), lane = int(lane_id());
-  const int kc = blockIdx.x;
-  const int64_t u = blockIdx.y;
-  const int32_t* list = idx + u * int64_t(L.nc) * k_sel;
-  const int beg = offs[u * (L.nc + 1) + kc], end = offs[u * (L.nc + 1) + kc + 1];
-  const int nq = end - beg;
-  const int npairs = (nq + 1) >> 1;
-  const int row0 = int(u * L.seqp);
+  // Tasks t = (unit u, key cube kc), t = u * nc + kc, handed out dynamically (a global
+  // counter: the transposed map's list lengths are very uneven, a static split leaves a
+  // long tail). The producer thread claims them and publishes each id through an
+  // 8-slot SMEM ring that every role reads in order (task_full / task_empty).
+  struct Task {
+    int64_t u;
+    int kc, beg, nq, npairs, row0;
+    const int32_t* list;
+  };
+  auto task = [&](int t) {
+    Task T;
+    T.u = t / L.nc;
+    T.kc = t - int(T.u) * L.nc;
+    T.list = idx + T.u * int64_t(L.nc) * k_sel;
+    T.beg = offs[T.u * (L.nc + 1) + T.kc];
+    T.nq = offs[T.u * (L.nc + 1) + T.kc + 1] - T.beg;
+    T.npairs = (T.nq + 1) >> 1;
+    T.row0 = int(T.u * L.seqp);
+    return T;
+  };
 
   if (warp == 10) tmem_alloc<512>(&sm->tmem);
   if (threadIdx.x == 0) {
     trace_ev(tr, 24, 4);
     mbar_init(&sm->kv_full, 1);
-    mbar_init(&sm->final_bar, 1);
+    mbar_init(&sm->kv_empty, 1);
+    for (int i = 0; i < kTaskRing; ++i) {
+      mbar_init(&sm->task_full[i], 1);
+      mbar_init(&sm->task_empty[i], kTaskConsumers);
+    }
     for (int g = 0; g < NG; ++g) {
       mbar_init(&sm->g_full[g], 1);
       mbar_init(&sm->g_empty[g], 1);
@@ -244,23 +282,20 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm->s_full[b], 1);
       mbar_init(&sm->dp_full[b], 1);
-      mbar_init(&sm->sd_free[b], kCompute);
+      mbar_init(&sm->acc_full[b], 1);
+      mbar_init(&sm->acc_free[b], kEpiThreads);
     }
     for (int b = 0; b < NPB; ++b) {
-      mbar_init(&sm->p_full[b], kCompute);
       mbar_init(&sm->ds_full[b], kCompute);
       mbar_init(&sm->ds_stored[b], 1);
     }
     fence_barrier_init();
   }
-  // a single-cube last pair reads rows 64..127 of its granules: make them finite once
-  // (later occupants leave loaded bf16 data behind); their P / dS rows are forced to 0
-  if ((nq & 1) && 2 * (npairs - 1) < NG) {
-    // items 2(npairs-1), 2(npairs-1)+1 take fresh granules 2(npairs-1).. (GranSeq: i < NG -> i)
-    const int g0 = 2 * (npairs - 1), ng = min(2, NG - g0);
-    for (int i = threadIdx.x; i < ng * C::kGran / 16; i += blockDim.x)
-      reinterpret_cast<uint4*>(sG + g0 * C::kGran)[i] = make_uint4(0, 0, 0, 0);
-  }
+  // A single-cube last pair reads rows 64..127 of its granules (their P / dS rows are
+  // forced to 0): later occupants leave finite bf16 data behind, so only the initial
+  // contents need clearing.
+  for (int i = threadIdx.x; i < NG * C::kGran / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sG)[i] = make_uint4(0, 0, 0, 0);
   if (D == 64)
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) reinterpret_cast<uint4*>(sZ)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
@@ -268,71 +303,114 @@ __global__ void __launch_bounds__(kKVThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = sm->tmem;
+  // consumer side of the task ring: one elected lane per consuming warp (or thread)
+  auto next_task = [&](int j, bool arrive) -> int {
+    const int slot = j & (kTaskRing - 1);
+    mbar_wait_sleep(&sm->task_full[slot], (j / kTaskRing) & 1);
+    const int t = sm->task_id[slot];
+    if (arrive) mbar_arrive(&sm->task_empty[slot]);
+    return t;
+  };
+  auto next_task_warp = [&](int j) -> int {
+    int t = 0;
+    if (lane == 0) t = next_task(j, true);
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
 
-  if (warp == 9 && lane == 1 && tr.buf != nullptr && int(blockIdx.x) == tr.cta_x && int(blockIdx.y) == tr.cta_y) {
-    // debug watcher: completion times of the four product groups of every pair
-    for (int p = 0; p < npairs; ++p) {  // only S completions: never lags behind
-      mbar_wait(&sm->s_full[p & 1], (p >> 1) & 1);
-      trace_ev(tr, 16, p);
-    }
-  } else if (warp == 9) {
-    // dS tile store: TMA-store the bf16 [64 q][64 keys] tiles of pair p for the dQ GEMM
-    // — tile (qcube, t) at rows ((u*nc + qcube)*k + t)*64, t = position of kc in
+  if (warp == 9) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kKVRegCtl));
+    // dS tile store: TMA-store the bf16 [64 q][64 keys] tiles of every pair for the dQ
+    // GEMM — tile (qcube, t) at rows ((u*nc + qcube)*k + t)*64, t = position of kc in
     // sel[qcube] — then release the buffer to the compute warps.
-    if (lane == 0 && ds_store) {
-      tma_prefetch_desc(&tm_ds);
-      const int64_t base = u * int64_t(L.nc) * k_sel;
-      for (int p = 0; p < npairs; ++p) {
-        const int b = p % NPB;
-        mbar_wait(&sm->ds_full[b], (p / NPB) & 1);
-        const int e = beg + 2 * p;
-        uint8_t* myS = sS + b * 16384;
-        tma_store_2d(&tm_ds, myS, 0, int((base + int64_t(list[e]) * k_sel + ds_pos[base + e]) * 64));
-        if (2 * p + 1 < nq)
-          tma_store_2d(&tm_ds, myS + 8192, 0, int((base + int64_t(list[e + 1]) * k_sel + ds_pos[base + e + 1]) * 64));
-        bulk_commit_group();
-        bulk_wait_group_read0();
-        mbar_arrive(&sm->ds_stored[b]);
+    if (lane == 0) {
+      if (ds_store) tma_prefetch_desc(&tm_ds);
+      int P = 0;  // global pair index
+      for (int j = 0;; ++j) {
+        const int t = next_task(j, true);
+        if (t < 0) break;
+        if (!ds_store) continue;
+        const Task T = task(t);
+        const int64_t base = T.u * int64_t(L.nc) * k_sel;
+        for (int p = 0; p < T.npairs; ++p, ++P) {
+          const int b = P % NPB;
+          mbar_wait(&sm->ds_full[b], (P / NPB) & 1);
+          const int e = T.beg + 2 * p;
+          uint8_t* myS = sS + b * 16384;
+          tma_store_2d(&tm_ds, myS, 0, int((base + int64_t(T.list[e]) * k_sel + ds_pos[base + e]) * 64));
+          if (2 * p + 1 < T.nq)
+            tma_store_2d(&tm_ds, myS + 8192, 0,
+                         int((base + int64_t(T.list[e + 1]) * k_sel + ds_pos[base + e + 1]) * 64));
+          bulk_commit_group();
+          bulk_wait_group_read0();
+          mbar_arrive(&sm->ds_stored[b]);
+        }
       }
       bulk_wait_group0();
     }
   } else if (warp == 8) {
-    if (lane == 0 && npairs > 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kKVRegCtl));
+    // producer: K / V of each task (once the previous task's last S / dP completed),
+    // then the task's Q / dO pair granules through the ring, which never drains
+    if (lane == 0) {
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_do);
-      mbar_arrive_expect_tx(&sm->kv_full, 2 * C::kCube);
-      for (int c = 0; c < C::kChunks; ++c) {
-        tma_load_2d(sK + c * C::kCubeChunk, &tm_k, &sm->kv_full, c * 64, row0 + kc * 64);
-        tma_load_2d(sV + c * C::kCubeChunk, &tm_v, &sm->kv_full, c * 64, row0 + kc * 64);
-      }
       GranSeq<NG> seq;
       uint32_t fills = 0;  // bit g: parity of the fills of granule g so far
-      for (int i = 0; i < 2 * npairs; ++i) {
-        const int p = i >> 1, g = seq.next(i);
-        const CUtensorMap* tm = (i & 1) ? &tm_do : &tm_q;
-        const int qa = list[beg + 2 * p];
-        const bool hb = 2 * p + 1 < nq;
-        const int qb = hb ? list[beg + 2 * p + 1] : 0;
-        mbar_wait(&sm->g_empty[g], ((fills >> g) & 1) ^ 1);
-        fills ^= 1u << g;
-        trace_ev(tr, 2, i);
-        mbar_arrive_expect_tx(&sm->g_full[g], (hb ? 2 : 1) * C::kCube);
-        uint8_t* dst = sG + g * C::kGran;
+      int i = 0, kvn = 0;  // global item index, non-empty tasks so far
+      for (int j = 0;; ++j) {
+        const int slot = j & (kTaskRing - 1);
+        mbar_wait(&sm->task_empty[slot], ((j / kTaskRing) & 1) ^ 1);
+        int t = atomicAdd(task_ctr, 1);
+        if (t >= ntasks) t = -1;
+        sm->task_id[slot] = t;
+        mbar_arrive(&sm->task_full[slot]);
+        if (t < 0) break;
+        const Task T = task(t);
+        if (T.npairs == 0) continue;
+        mbar_wait(&sm->kv_empty, (kvn & 1) ^ 1);
+        ++kvn;
+        mbar_arrive_expect_tx(&sm->kv_full, 2 * C::kCube);
         for (int c = 0; c < C::kChunks; ++c) {
-          tma_load_2d(dst + c * C::kPairChunk, tm, &sm->g_full[g], c * 64, row0 + qa * 64);
-          if (hb) tma_load_2d(dst + c * C::kPairChunk + 8192, tm, &sm->g_full[g], c * 64, row0 + qb * 64);
+          tma_load_2d(sK + c * C::kCubeChunk, &tm_k, &sm->kv_full, c * 64, T.row0 + T.kc * 64);
+          tma_load_2d(sV + c * C::kCubeChunk, &tm_v, &sm->kv_full, c * 64, T.row0 + T.kc * 64);
+        }
+        for (int li = 0; li < 2 * T.npairs; ++li, ++i) {
+          const int p = li >> 1, g = seq.next(i);
+          const CUtensorMap* tm = (li & 1) ? &tm_do : &tm_q;
+          const int qa = T.list[T.beg + 2 * p];
+          const bool hb = 2 * p + 1 < T.nq;
+          const int qb = hb ? T.list[T.beg + 2 * p + 1] : 0;
+          mbar_wait(&sm->g_empty[g], ((fills >> g) & 1) ^ 1);
+          fills ^= 1u << g;
+          trace_ev(tr, 2, i);
+          mbar_arrive_expect_tx(&sm->g_full[g], (hb ? 2 : 1) * C::kCube);
+          uint8_t* dst = sG + g * C::kGran;
+          for (int c = 0; c < C::kChunks; ++c) {
+            tma_load_2d(dst + c * C::kPairChunk, tm, &sm->g_full[g], c * 64, T.row0 + qa * 64);
+            if (hb) tma_load_2d(dst + c * C::kPairChunk + 8192, tm, &sm->g_full[g], c * 64, T.row0 + qb * 64);
+          }
         }
       }
     }
   } else if (warp == 11) {
-    // load watcher: waits for each streamed granule's TMA, then meets the issuer at a
-    // named barrier (it runs at most one item ahead per barrier ID)
-    if (npairs > 0) {
-      GranSeq<NG> seq;
-      uint32_t fills = 0;
-      for (int i = 0; i < 2 * npairs; ++i) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kKVRegCtl));
+    // load watcher: waits for each streamed granule's TMA (and each task's K / V), then
+    // meets the issuer at a named barrier, in consumption order
+    GranSeq<NG> seq;
+    uint32_t fills = 0;
+    int i = 0, kvn = 0;
+    for (int j = 0;; ++j) {
+      const int t = next_task_warp(j);
+      if (t < 0) break;
+      const Task T = task(t);
+      if (T.npairs == 0) continue;
+      for (int li = 0; li < 2 * T.npairs; ++li, ++i) {
+        if (li == 0) {
+          mbar_wait_warp(&sm->kv_full, kvn & 1);
+          ++kvn;
+        }
         const int g = seq.next(i);
         mbar_wait_warp(&sm->g_full[g], (fills >> g) & 1);
         fills ^= 1u << g;
@@ -340,227 +418,263 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       }
     }
   } else if (warp == 10) {
-    if (npairs > 0) {  // whole warp: warp-uniform issue, one elected lane issues
-      constexpr uint32_t idSD = make_idesc_bf16(128, 64, false, false);
-      constexpr uint32_t idG = make_idesc_bf16(128, 64, true, true);
-      const uint32_t aG = smem_u32(sG), aP = smem_u32(sP), aS = smem_u32(sS);  // NPB = 1 (static_assert)
-      // descriptor bases; K-steps advance the start address (+32 B = +2 encoded)
-      const uint64_t dK0 = make_sdesc_sw128(smem_u32(sK), 16, 1024), dV0 = make_sdesc_sw128(smem_u32(sV), 16, 1024);
-      const uint64_t dG0 = make_sdesc_sw128(aG, 16, 1024);
-      GranSeq<NG> seq;
-      // granules of Q / dO of the two pairs in flight, by pair parity (scalars: a
-      // runtime-indexed array would live in local memory, whose loads the SS MMA
-      // operand stream starves). The issuing warp runs nearly in lock-step with the
-      // tensor pipe, so everything between two product groups is kept minimal.
-      int gq0 = 0, gq1 = 0, go0 = 0, go1 = 0;
-      mbar_wait_warp(&sm->kv_full, 0);
-      // S(n) = Qpair.K^T and dP(n) = dOpair.V^T into TMEM buffer n&1
-      auto issue_s = [&](int n) {
-        const int b = n & 1;
-        const int g0 = seq.next(2 * n);
-        if (b) gq1 = g0; else gq0 = g0;
-        const uint64_t q0 = dG0 + uint64_t((g0 * C::kGran) >> 4);
-        if (lane == 0) trace_ev(tr, 12, n);
-        if (n >= 2) named_bar_b(kBarSdFree + b, kCompute + 32);
-        named_bar_b(kBarGran, 64);
-        tc_fence_after();
-        if (lane == 0) trace_ev(tr, 13, n);
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kKVRegCtl));
+    // MMA issuer (whole warp: warp-uniform issue, one elected lane issues)
+    constexpr uint32_t idSD = make_idesc_bf16(128, 64, false, false);
+    constexpr uint32_t idG = make_idesc_bf16(128, 64, true, true);
+    const uint32_t aG = smem_u32(sG), aP = smem_u32(sP), aS = smem_u32(sS);  // NPB = 1 (static_assert)
+    // descriptor bases; K-steps advance the start address (+32 B = +2 encoded)
+    const uint64_t dK0 = make_sdesc_sw128(smem_u32(sK), 16, 1024), dV0 = make_sdesc_sw128(smem_u32(sV), 16, 1024);
+    const uint64_t dG0 = make_sdesc_sw128(aG, 16, 1024);
+    const uint64_t dP0 = make_sdesc_sw128(aP, 8192, 1024), dS0 = make_sdesc_sw128(aS, 8192, 1024);
+    const uint32_t lboZ = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - aG;  // minus granule offset
+    GranSeq<NG> seq;
+    // granules of Q / dO of the two pairs in flight, by pair parity (scalars: a
+    // runtime-indexed array would live in local memory, whose loads the SS MMA
+    // operand stream starves). The issuing warp runs nearly in lock-step with the
+    // tensor pipe, so everything between two product groups is kept minimal.
+    int gq0 = 0, gq1 = 0, go0 = 0, go1 = 0;
+    int P = 0, acn = 0;  // global index of pair 0 of the task, non-empty tasks so far
+    // S(n) = Qpair.K^T and dP(n) = dOpair.V^T into TMEM buffer n&1 (n: global pair)
+    auto issue_s = [&](int n) {
+      const int b = n & 1;
+      const int g0 = seq.next(2 * n);
+      if (b) gq1 = g0; else gq0 = g0;
+      const uint64_t q0 = dG0 + uint64_t((g0 * C::kGran) >> 4);
+      if (n >= 2) named_bar_b(kBarSdFree + b, kCompute + 32);
+      named_bar_b(kBarGran, 64);
+      tc_fence_after();
 #pragma unroll
-        for (int s = 0; s < D / 16; ++s)
-          umma_bf16_warp(tbase + b * 64, q0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
-                         dK0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
-        if (lane == 0) trace_ev(tr, 14, n);
-        umma_commit_warp(&sm->s_full[b]);
-      };
-      auto issue_dp = [&](int n) {
-        const int b = n & 1;
-        const int g1 = seq.next(2 * n + 1);
-        if (b) go1 = g1; else go0 = g1;
-        const uint64_t o0 = dG0 + uint64_t((g1 * C::kGran) >> 4);
-        if (lane == 0) trace_ev(tr, 20, n);
-        named_bar_b(kBarGran, 64);
-        tc_fence_after();
-        if (lane == 0) trace_ev(tr, 21, n);
+      for (int s = 0; s < D / 16; ++s)
+        umma_bf16_warp(tbase + b * 64, q0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
+                       dK0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+      umma_commit_warp(&sm->s_full[b]);
+    };
+    auto issue_dp = [&](int n) {
+      const int b = n & 1;
+      const int g1 = seq.next(2 * n + 1);
+      if (b) go1 = g1; else go0 = g1;
+      const uint64_t o0 = dG0 + uint64_t((g1 * C::kGran) >> 4);
+      named_bar_b(kBarGran, 64);
+      tc_fence_after();
 #pragma unroll
-        for (int s = 0; s < D / 16; ++s)
-          umma_bf16_warp(tbase + 128 + b * 64, o0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
-                         dV0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
-        if (lane == 0) trace_ev(tr, 22, n);
-        umma_commit_warp(&sm->dp_full[b]);
-      };
-      const uint64_t dP0 = make_sdesc_sw128(aP, 8192, 1024), dS0 = make_sdesc_sw128(aS, 8192, 1024);
-      const uint32_t lboZ = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - aG;  // minus granule offset
+      for (int s = 0; s < D / 16; ++s)
+        umma_bf16_warp(tbase + 128 + b * 64, o0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
+                       dV0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+      umma_commit_warp(&sm->dp_full[b]);
+    };
+    for (int j = 0;; ++j) {
+      const int t = next_task_warp(j);
+      if (t < 0) break;
+      const int npairs = task(t).npairs;
+      if (npairs == 0) continue;
+      const int ab = acn & 1;
+      const uint32_t tV = tbase + 256 + ab * 128, tK = tV + 64;  // this task's dV^T / dK^T accumulators
+      if (lane == 0) trace_ev(tr, 12, j);
       // Fixed software-pipelined order per pair p:  S(p+1), dV(p), dP(p+1), dK(p).
-      // The exp / dS math of a pair runs a full period ahead of its dV / dK, and the
-      // granule of dO(p) is released (after dV(p)) early enough to refill dO(p+2)
-      // with NG = 5 (a load takes ~1200 cycles, a product group ~400).
-      issue_s(0);
-      issue_dp(0);
+      // The exp / dS math of a pair runs a full period ahead of its dV / dK. K / V of
+      // the next task are released after the last dP (kv_empty), so their load
+      // overlaps this task's last dV / dK groups.
+      issue_s(P);
+      issue_dp(P);
+      if (npairs == 1) umma_commit_warp(&sm->kv_empty);
       for (int p = 0; p < npairs; ++p) {
-        const int b = p & 1;
-        if (p + 1 < npairs) issue_s(p + 1);
+        const int n = P + p, b = n & 1;
+        if (p + 1 < npairs) issue_s(n + 1);
         {
           const int g = b ? go1 : go0;
           const uint32_t goff = uint32_t(g * C::kGran);
           const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
-          if (lane == 0) trace_ev(tr, 17, p);
+          if (p == 0 && acn >= 2) mbar_wait_warp(&sm->acc_free[ab], ((acn >> 1) & 1) ^ 1);  // epilogue of task-2 read it
           named_bar_b(kBarPFull, kCompute + 32);
           tc_fence_after();
-          if (lane == 0) trace_ev(tr, 18, p);
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_bf16_warp(tbase + 256, da + uint64_t(s * 128), dP0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
-          if (lane == 0) trace_ev(tr, 19, p);
+            umma_bf16_warp(tV, da + uint64_t(s * 128), dP0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
           umma_commit_warp(&sm->g_empty[g]);
         }
-        if (p + 1 < npairs) issue_dp(p + 1);
+        if (p + 1 < npairs) {
+          issue_dp(n + 1);
+          if (p + 2 == npairs) umma_commit_warp(&sm->kv_empty);
+        }
         {
           const int g = b ? gq1 : gq0;
           const uint32_t goff = uint32_t(g * C::kGran);
           const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
-          if (lane == 0) trace_ev(tr, 25, p);
           named_bar_b(kBarDsFull, kCompute + 32);
           tc_fence_after();
-          if (lane == 0) trace_ev(tr, 26, p);
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_bf16_warp(tbase + 320, da + uint64_t(s * 128), dS0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
-          if (lane == 0) trace_ev(tr, 27, p);
+            umma_bf16_warp(tK, da + uint64_t(s * 128), dS0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
           umma_commit_warp(&sm->g_empty[g]);
         }
       }
-      umma_commit_warp(&sm->final_bar);
+      umma_commit_warp(&sm->acc_full[ab]);
+      if (lane == 0) trace_ev(tr, 13, j);
+      P += npairs;
+      ++acn;
+    }
+    // consume the compute warps' last S-buffer releases (no later S waits on them)
+    for (int n = P >= 2 ? P - 2 : 0; n < P; ++n) named_bar_b(kBarSdFree + (n & 1), kCompute + 32);
+  } else if (warp >= 12) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kKVRegEpi));
+    // ---------------------------------------------------------------- epilogue warps
+    // dV^T / dK^T of task j: TMEM lane = d, column = key token of the cube. Each
+    // thread reads its d row in 32-column slices and stores bf16 scalars (one warp
+    // instruction = 64 contiguous bytes of a token row), adding the cube-level
+    // mean-unpool term; the whole epilogue overlaps the next task's products.
+    const int dl = (warp & 3) * 32 + lane;
+    const uint32_t lrow = tbase + (uint32_t((warp & 3) * 32) << 16);
+    const float inv = 1.0f / float(L.cube);
+    int acn = 0;
+    for (int j = 0;; ++j) {
+      const int t = next_task_warp(j);
+      if (t < 0) break;
+      const Task T = task(t);
+      const int64_t o = (T.u * L.nc + T.kc) * D + dl;
+      const float xk = (dkc && dl < D) ? dkc[o] * inv : 0.f, xv = (dvc && dl < D) ? dvc[o] * inv : 0.f;
+      // output rows of tokens lane and lane + 32 of the cube (-1: pad token)
+      const int64_t r0 = cube_out_row(L, T.u, T.kc, lane, raster), r1 = cube_out_row(L, T.u, T.kc, lane + 32, raster);
+      const bool acc = T.npairs > 0;
+      const int ab = acn & 1;
+      if (acc) {
+        mbar_wait_sleep(&sm->acc_full[ab], (acn >> 1) & 1);
+        tc_fence_after();
+      }
+#pragma unroll 1
+      for (int t = 0; t < 2; ++t) {  // t = 0: dV, t = 1: dK
+        __nv_bfloat16* dst = t ? dk : dv;
+        const float sc = t ? scale : 1.f, x = t ? xk : xv;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {  // key columns [32h, 32h + 32)
+          float a[32];
+          if (acc) {
+            tmem_ld32(lrow + 256 + ab * 128 + t * 64 + h * 32, a);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) a[i] = 0.f;
+          }
+          const int64_t rr = h ? r1 : r0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int64_t row = __shfl_sync(0xffffffffu, rr, i);
+            if (row >= 0 && dl < D) dst[row * D + dl] = __float2bfloat16_rn(fmaf(a[i], sc, x));
+          }
+        }
+      }
+      if (threadIdx.x == 12 * 32) trace_ev(tr, 14, j);
+      if (acc) {
+        tc_fence_before();
+        mbar_arrive(&sm->acc_free[ab]);
+        ++acn;
+      }
     }
   } else if (warp < 8) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kKVRegCmp));
     // 8 compute warps on every pair: warp w owns TMEM lanes 32*(w%4).. (query rows)
     // and key columns [32*ch, 32*ch+32), ch = w/4.
     const int ch = warp >> 2;
     const int ql = (warp & 3) * 32 + lane;  // query lane within the pair
     const uint32_t lrow = tbase + (uint32_t((warp & 3) * 32) << 16);
-    // prefetch the unpool rows now: the epilogue then has no dependent global loads
-    if (threadIdx.x < D) {
-      const int64_t o = (u * L.nc + kc) * D + threadIdx.x;
-      sm->xk[threadIdx.x] = dkc ? dkc[o] : 0.f;
-      sm->xv[threadIdx.x] = dvc ? dvc[o] : 0.f;
-    } else if (threadIdx.x < D + 64) {
-      sm->rows[threadIdx.x - D] = cube_out_row(L, u, kc, threadIdx.x - D, raster);
-    }
-    // lse / delta of this thread's query row, prefetched one pair ahead (two dependent
-    // global loads per pair would otherwise sit on the compute path)
-    auto row_stats = [&](int pp, float& l2, float& dlt) {
-      l2 = 0.f;
-      dlt = 0.f;
-      if (pp < npairs && (ql < 64 || 2 * pp + 1 < nq)) {
-        const int qcube = list[beg + 2 * pp + (ql >> 6)];
-        const int64_t trow = int64_t(row0) + int64_t(qcube) * 64 + (ql & 63);
-        l2 = lse[trow];
-        dlt = delta[trow];
-      }
-    };
-    float nl2, ndl;
-    row_stats(0, nl2, ndl);
-    // The P / dS buffers of pair p-1 are free once dV(p-1) / dK(p-1) complete, which is
-    // exactly when the granules of dO(p-1) / Q(p-1) are released: wait on those g_empty
+    // The P / dS buffers of pair P-1 are free once dV(P-1) / dK(P-1) complete, which is
+    // exactly when the granules of dO(P-1) / Q(P-1) are released: wait on those g_empty
     // phases (same GranSeq as producer / issuer) instead of extra per-pair commits.
     GranSeq<NG> gseq;
     uint32_t uses = 0;           // bit g: parity of the fills of granule g so far
-    int pq_g = 0, po_g = 0;      // granules of Q(p-1), dO(p-1)
+    int pq_g = 0, po_g = 0;      // granules of Q(P-1), dO(P-1)
     uint32_t pq_par = 0, po_par = 0;
-    for (int p = 0; p < npairs; ++p) {
-      const int cq_g = gseq.next(2 * p), co_g = gseq.next(2 * p + 1);
-      const uint32_t cq_par = (uses >> cq_g) & 1u;
-      uses ^= 1u << cq_g;
-      const uint32_t co_par = (uses >> co_g) & 1u;
-      uses ^= 1u << co_g;
-      const int b = p & 1, pb = p % NPB, use = p / NPB;
-      uint8_t* myP = sP + pb * 16384;
-      uint8_t* myS = sS + pb * 16384;
-      const bool valid = ql < 64 || (2 * p + 1 < nq);  // warp-uniform
-      const float lse2 = nl2 * 1.4426950408889634f, dl = ndl;
-      row_stats(p + 1, nl2, ndl);
-      mbar_wait_sleep(&sm->s_full[b], (p >> 1) & 1);
-      if (threadIdx.x == 0) trace_ev(tr, 5, p);
-      tc_fence_after();
-      float pf[32];
-      uint32_t pk[16];
-      {
-        uint32_t rs[32];
-        tmem_ld32_raw(lrow + b * 64 + ch * 32, rs);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float a, c;
-          f2_unpack(ffma2(f2(__uint_as_float(rs[2 * j]), __uint_as_float(rs[2 * j + 1])), f2(scale_log2, scale_log2),
-                          f2(-lse2, -lse2)),
-                    a, c);
-          pf[2 * j] = valid ? ex2b(a) : 0.f;
-          pf[2 * j + 1] = valid ? ex2b(c) : 0.f;
+    int P = 0;
+    for (int j = 0;; ++j) {
+      const int t = next_task_warp(j);
+      if (t < 0) break;
+      const Task T = task(t);
+      // lse / delta of this thread's query row, prefetched one pair ahead (two dependent
+      // global loads per pair would otherwise sit on the compute path)
+      auto row_stats = [&](int pp, float& l2, float& dlt) {
+        l2 = 0.f;
+        dlt = 0.f;
+        if (pp < T.npairs && (ql < 64 || 2 * pp + 1 < T.nq)) {
+          const int qcube = T.list[T.beg + 2 * pp + (ql >> 6)];
+          const int64_t trow = int64_t(T.row0) + int64_t(qcube) * 64 + (ql & 63);
+          l2 = lse[trow];
+          dlt = delta[trow];
         }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(pf[2 * j], pf[2 * j + 1]);
-      }
-      if (threadIdx.x == 0) trace_ev(tr, 6, p);
-      if (p >= 1) mbar_wait_sleep(&sm->g_empty[po_g], po_par);  // dV(p-1) done: P buffer free
-      if (threadIdx.x == 0) trace_ev(tr, 8, p);
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        *reinterpret_cast<uint4*>(myP + sw128_offset(ql, (ch * 4 + c) * 16)) =
-            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      fence_proxy_async_smem();
-      named_bar_arrive(kBarPFull, kCompute + 32);
-      mbar_wait_sleep(&sm->dp_full[b], (p >> 1) & 1);
-      if (threadIdx.x == 0) trace_ev(tr, 9, p);
-      tc_fence_after();
-      {
-        uint32_t rd[32];
-        tmem_ld32_raw(lrow + 128 + b * 64 + ch * 32, rd);
-        tmem_wait_ld();
-        tc_fence_before();
-        named_bar_arrive(kBarSdFree + b, kCompute + 32);
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
+      };
+      float nl2, ndl;
+      row_stats(0, nl2, ndl);
+      for (int p = 0; p < T.npairs; ++p, ++P) {
+        const int cq_g = gseq.next(2 * P), co_g = gseq.next(2 * P + 1);
+        const uint32_t cq_par = (uses >> cq_g) & 1u;
+        uses ^= 1u << cq_g;
+        const uint32_t co_par = (uses >> co_g) & 1u;
+        uses ^= 1u << co_g;
+        const int b = P & 1, pb = P % NPB, use = P / NPB;
+        uint8_t* myP = sP + pb * 16384;
+        uint8_t* myS = sS + pb * 16384;
+        const bool valid = ql < 64 || (2 * p + 1 < T.nq);  // warp-uniform
+        const float lse2 = nl2 * 1.4426950408889634f, dl = ndl;
+        row_stats(p + 1, nl2, ndl);
+        mbar_wait_sleep(&sm->s_full[b], (P >> 1) & 1);
+        if (threadIdx.x == 0) trace_ev(tr, 5, P);
+        tc_fence_after();
+        float pf[32];
+        uint32_t pk[16];
         {
-          float a, c;
-          f2_unpack(fmul2(f2(pf[2 * j], pf[2 * j + 1]),
-                          fadd2(f2(__uint_as_float(rd[2 * j]), __uint_as_float(rd[2 * j + 1])), f2(-dl, -dl))),
-                    a, c);
-          pk[j] = pack_bf16(a, c);
-        }
-      }
-      if (threadIdx.x == 0) trace_ev(tr, 10, p);
-      if (p >= NPB) {
-        mbar_wait_sleep(&sm->g_empty[pq_g], pq_par);                       // dK(p-1) done: dS buffer free
-        if (ds_store) mbar_wait_sleep(&sm->ds_stored[pb], (use - 1) & 1);  // and its dS store read it
-      }
-      if (threadIdx.x == 0) trace_ev(tr, 11, p);
+          uint32_t rs[32];
+          tmem_ld32_raw(lrow + b * 64 + ch * 32, rs);
+          tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        *reinterpret_cast<uint4*>(myS + sw128_offset(ql, (ch * 4 + c) * 16)) =
-            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      fence_proxy_async_smem();
-      named_bar_arrive(kBarDsFull, kCompute + 32);
-      mbar_arrive(&sm->ds_full[pb]);  // for the dS store warp
-      if (threadIdx.x == 0) trace_ev(tr, 7, p);
-      pq_g = cq_g, pq_par = cq_par, po_g = co_g, po_par = co_par;
-    }
-    // ---------------------------------------------------------------- epilogue
-    float* stK = reinterpret_cast<float*>(sG);                 // [64][D] fp32
-    float* stV = reinterpret_cast<float*>(sG + 64 * D * 4);    // [64][D] fp32
-    if (npairs > 0) {
-      mbar_wait_sleep(&sm->final_bar, 0);
-      if (threadIdx.x == 0) trace_ev(tr, 24, 1);
-      tc_fence_after();
-      if (ql < D) {  // warps 0-3 stage dK^T, warps 4-7 dV^T
-        stage_cols<D>(lrow + (ch ? 256 : 320), 0, ch ? stV : stK, ql, ch ? 1.f : scale);
-        stage_cols<D>(lrow + (ch ? 256 : 320), 32, ch ? stV : stK, ql, ch ? 1.f : scale);
+          for (int jj = 0; jj < 16; ++jj) {
+            float a, c;
+            f2_unpack(ffma2(f2(__uint_as_float(rs[2 * jj]), __uint_as_float(rs[2 * jj + 1])),
+                            f2(scale_log2, scale_log2), f2(-lse2, -lse2)),
+                      a, c);
+            pf[2 * jj] = valid ? ex2b(a) : 0.f;
+            pf[2 * jj + 1] = valid ? ex2b(c) : 0.f;
+          }
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) pk[jj] = pack_bf16(pf[2 * jj], pf[2 * jj + 1]);
+        }
+        if (threadIdx.x == 0) trace_ev(tr, 6, P);
+        if (P >= 1) mbar_wait_sleep(&sm->g_empty[po_g], po_par);  // dV(P-1) done: P buffer free
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<uint4*>(myP + sw128_offset(ql, (ch * 4 + c) * 16)) =
+              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        fence_proxy_async_smem();
+        named_bar_arrive(kBarPFull, kCompute + 32);
+        mbar_wait_sleep(&sm->dp_full[b], (P >> 1) & 1);
+        tc_fence_after();
+        {
+          uint32_t rd[32];
+          tmem_ld32_raw(lrow + 128 + b * 64 + ch * 32, rd);
+          tmem_wait_ld();
+          tc_fence_before();
+          named_bar_arrive(kBarSdFree + b, kCompute + 32);
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            float a, c;
+            f2_unpack(fmul2(f2(pf[2 * jj], pf[2 * jj + 1]),
+                            fadd2(f2(__uint_as_float(rd[2 * jj]), __uint_as_float(rd[2 * jj + 1])), f2(-dl, -dl))),
+                      a, c);
+            pk[jj] = pack_bf16(a, c);
+          }
+        }
+        if (P >= NPB) {
+          mbar_wait_sleep(&sm->g_empty[pq_g], pq_par);                       // dK(P-1) done: dS buffer free
+          if (ds_store) mbar_wait_sleep(&sm->ds_stored[pb], (use - 1) & 1);  // and its dS store read it
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<uint4*>(myS + sw128_offset(ql, (ch * 4 + c) * 16)) =
+              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        fence_proxy_async_smem();
+        named_bar_arrive(kBarDsFull, kCompute + 32);
+        if (ds_store) mbar_arrive(&sm->ds_full[pb]);  // for the dS store warp
+        if (threadIdx.x == 0) trace_ev(tr, 7, P);
+        pq_g = cq_g, pq_par = cq_par, po_g = co_g, po_par = co_par;
       }
     }
-    named_bar_b(1, kCompute);
-    write_rows_x<D>(L, u, kc, npairs > 0 ? stK : nullptr, dkc ? sm->xk : nullptr, sm->rows, dk, threadIdx.x,
-                    kCompute);
-    write_rows_x<D>(L, u, kc, npairs > 0 ? stV : nullptr, dvc ? sm->xv : nullptr, sm->rows, dv, threadIdx.x,
-                    kCompute);
-    if (threadIdx.x == 0) trace_ev(tr, 24, 2);
   }
   tc_fence_before();
   __syncthreads();
@@ -1026,9 +1140,22 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
     const size_t smem = KVCfg<D>::kTiles + sizeof(KVSmall) + 1024;
     auto kern = fine_dkdv_sm100_kernel<D>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    kern<<<grid, kKVThreads, smem, st>>>(tq, tk, tv, tdo, L, int(top_k), scale, scale_log2, lse, delta, offs, idx,
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ntasks = bh * Lh.nc;  // persistent: one CTA per SM over the (unit, key cube) tasks
+    int* ctr = store_ds ? reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + ((tiles * (8192 + 4) + 15) & ~int64_t(15)))
+                        : nullptr;
+    if (!ctr) {
+      void* sym = nullptr;
+      cudaGetSymbolAddress(&sym, g_dkdv_task_ctr);
+      ctr = static_cast<int*>(sym);
+    }
+    cudaMemsetAsync(ctr, 0, sizeof(int), st);
+    kern<<<unsigned(std::min<int64_t>(ntasks, sms)), kKVThreads, smem, st>>>(
+        tq, tk, tv, tdo, L, int(ntasks), int(top_k), scale, scale_log2, lse, delta, offs, idx,
                                          dkc, dvc, raster, static_cast<__nv_bfloat16*>(dk),
-                                         static_cast<__nv_bfloat16*>(dv), tds, pos, store_ds ? 1 : 0,
+                                         static_cast<__nv_bfloat16*>(dv), tds, pos, store_ds ? 1 : 0, ctr,
                                          debug_trace());
     int rc = kernel_status("fine_dkdv_sm100_kernel");
     if (rc) return rc;
@@ -1046,7 +1173,7 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
 
 size_t fine_backward_ws_bytes(const vsa_layout_t& L, int64_t bh, int64_t top_k) {
   const int64_t tiles = bh * L.nc * top_k;
-  return size_t(tiles) * (8192 + 4);
+  return size_t(tiles) * (8192 + 4) + 256;  // dS tiles, CSR positions, dK/dV task counter
 }
 
 int launch_fine_backward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, const void* q, const void* k,
