@@ -174,8 +174,10 @@ int vsa_coarse_backward(const vsa_layout_t* layout, int64_t bh, int64_t d, const
  * (coarse.hpp:164-178, mean mode) and the grad sum of vsa_backward (vsa.hpp:182-187):
  *   dq = dQ_fine + dqc/cube (broadcast), dk, dv likewise; dqc/dkc/dvc may be NULL.
  *   dof, lse, delta as produced by the forward / prologue; selT_* from the
- *   coarse stage or vsa_selection_transpose. Deterministic (no atomics): dQ per
- *   query cube, dK/dV per key cube over the transposed map, q-cubes ascending.
+ *   coarse stage or vsa_selection_transpose. Deterministic (no atomics on any
+ *   gradient): dQ per query cube, dK/dV per key cube over the transposed map,
+ *   q-cubes ascending (key cubes are handed to CTAs by a counter in the workspace;
+ *   each is still computed by one CTA in a fixed order).
  *   Unselected key cubes get exactly zero fine gradient (test_fine.cpp:149-169).
  * raster != 0 writes dq/dk/dv in raster order (padded rows dropped).
  * workspace (device, >= vsa_fine_backward_workspace_bytes, may be NULL): with it the
@@ -186,7 +188,8 @@ int vsa_fine_backward(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t
                       int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx, const float* dqc,
                       const float* dkc, const float* dvc, int32_t raster, int32_t flags, void* dq, void* dk,
                       void* dv, void* workspace, size_t workspace_bytes, void* stream);
-/* Workspace size for the dS-materialising backward: B*H*nc*top_k tiles x (8 KiB + 4 B). */
+/* Workspace size for the dS-materialising backward: B*H*nc*top_k tiles x (8 KiB + 4 B),
+ * plus 256 B for the dK/dV task counter. */
 size_t vsa_fine_backward_workspace_bytes(const vsa_layout_t* layout, int64_t bh, int64_t top_k);
 
 /* Max-pool unpool (coarse.hpp:172-176): adds dxc[cube][j] to the first argmax

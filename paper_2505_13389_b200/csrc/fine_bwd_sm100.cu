@@ -204,8 +204,6 @@ struct KVCfg {
 };
 
 constexpr int kTaskRing = 8;
-// task counter of launches without a workspace (the dS fallback path)
-__device__ int g_dkdv_task_ctr;
 // task-ring readers: dS-store thread, watcher, issuer, 8 compute warps, 4 epilogue warps
 constexpr int kTaskConsumers = 1 + 1 + 1 + 8 + 4;
 
@@ -362,7 +360,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       for (int j = 0;; ++j) {
         const int slot = j & (kTaskRing - 1);
         mbar_wait(&sm->task_empty[slot], ((j / kTaskRing) & 1) ^ 1);
-        int t = atomicAdd(task_ctr, 1);
+        // without a workspace (no counter): static round-robin hand-out
+        int t = task_ctr ? atomicAdd(task_ctr, 1) : int(blockIdx.x) + j * int(gridDim.x);
         if (t >= ntasks) t = -1;
         sm->task_id[slot] = t;
         mbar_arrive(&sm->task_full[slot]);
@@ -1146,12 +1145,7 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
     const int64_t ntasks = bh * Lh.nc;  // persistent: one CTA per SM over the (unit, key cube) tasks
     int* ctr = store_ds ? reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + ((tiles * (8192 + 4) + 15) & ~int64_t(15)))
                         : nullptr;
-    if (!ctr) {
-      void* sym = nullptr;
-      cudaGetSymbolAddress(&sym, g_dkdv_task_ctr);
-      ctr = static_cast<int*>(sym);
-    }
-    cudaMemsetAsync(ctr, 0, sizeof(int), st);
+    if (ctr) cudaMemsetAsync(ctr, 0, sizeof(int), st);
     kern<<<unsigned(std::min<int64_t>(ntasks, sms)), kKVThreads, smem, st>>>(
         tq, tk, tv, tdo, L, int(ntasks), int(top_k), scale, scale_log2, lse, delta, offs, idx,
                                          dkc, dvc, raster, static_cast<__nv_bfloat16*>(dk),

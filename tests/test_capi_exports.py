@@ -71,7 +71,8 @@ def test_invalid_arguments_are_rejected_without_a_gpu(lib):
     # k out of range -> VSA_EINVAL with the reference's message (coarse.hpp:79-80)
     rc = lib.vsa_coarse_forward(C.byref(L), 1, 64, None, None, None, 0, None, None, None, None, None, None, None)
     assert rc < 0 and b"k must be in [1, num_cubes]" in lib.vsa_last_error()
-    assert lib.vsa_fine_backward_workspace_bytes(C.byref(L), 2, 4) == 2 * 32 * 4 * (8192 + 4)
+    # bf16 dS tiles + CSR positions + the dK/dV task counter
+    assert lib.vsa_fine_backward_workspace_bytes(C.byref(L), 2, 4) == 2 * 32 * 4 * (8192 + 4) + 256
 
 
 def test_bench_reference_arm_runs_on_cpu():
