@@ -172,41 +172,54 @@ __global__ void sel_to_bitmap_kernel(int64_t rows, int nc, int k, const int32_t*
   }
 }
 
-// grid bh, block 256: counts, exclusive scan, ordered fill.
+// Transposed map from the bitmap: grid (ceil(nc / 8), bh), one warp per key cube kc.
+// Each block recounts the key cubes before its own (popc over the bitmap rows, a few
+// KB from L2) for its base offset, scans its 8 warps' counts, and every warp writes
+// its query cubes in ascending order (lane = bitmap word, warp-scanned offsets).
 __global__ void __launch_bounds__(256) bitmap_to_csr_kernel(int nc, int words, const uint32_t* __restrict__ bitmap,
                                                            int32_t* __restrict__ offs, int32_t* __restrict__ idx,
                                                            int64_t idx_stride) {
-  extern __shared__ int32_t cnt[];  // [nc + 1]
-  const int64_t u = blockIdx.x;
+  __shared__ int red[8], wcnt[8];
+  const int64_t u = blockIdx.y;
   const uint32_t* bm = bitmap + u * nc * int64_t(words);
-  for (int kc = threadIdx.x; kc < nc; kc += blockDim.x) {
-    int c = 0;
-    for (int w = 0; w < words; ++w) c += __popc(bm[int64_t(kc) * words + w]);
-    cnt[kc] = c;
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kc0 = blockIdx.x * 8, kc = kc0 + warp;
+  // base = number of set bits in rows [0, kc0)
+  int part = 0;
+  for (int64_t e = threadIdx.x; e < int64_t(kc0) * words; e += blockDim.x) part += __popc(bm[e]);
+  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) red[warp] = part;
+  int c = 0;  // this warp's key cube count
+  if (kc < nc)
+    for (int w = lane; w < words; w += 32) c += __popc(bm[int64_t(kc) * words + w]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) wcnt[warp] = c;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int run = 0;
-    for (int kc = 0; kc < nc; ++kc) {
-      const int c = cnt[kc];
-      cnt[kc] = run;
-      run += c;
-    }
-    cnt[nc] = run;
-  }
-  __syncthreads();
+  int base = 0;
+  for (int i = 0; i < 8; ++i) base += red[i];
+  for (int i = 0; i < warp; ++i) base += wcnt[i];
   int32_t* o = offs + u * (nc + 1);
-  for (int kc = threadIdx.x; kc <= nc; kc += blockDim.x) o[kc] = cnt[kc];
-  int32_t* dst = idx + u * idx_stride;
-  for (int kc = threadIdx.x; kc < nc; kc += blockDim.x) {
-    int p = cnt[kc];
-    for (int w = 0; w < words; ++w) {
-      uint32_t bits = bm[int64_t(kc) * words + w];
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        dst[p++] = w * 32 + b;
+  if (kc < nc) {
+    if (lane == 0) o[kc] = base;
+    if (kc == nc - 1 && lane == 0) o[nc] = base + c;
+    int32_t* dst = idx + u * idx_stride;
+    int run = base;
+    for (int w0 = 0; w0 < words; w0 += 32) {
+      const int w = w0 + lane;
+      uint32_t bits = w < words ? bm[int64_t(kc) * words + w] : 0u;
+      const int n = __popc(bits);
+      int incl = n;  // inclusive warp scan of the word counts
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
       }
+      int p = run + incl - n;
+      while (bits) {
+        const int bt = __ffs(bits) - 1;
+        bits &= bits - 1;
+        dst[p++] = w * 32 + bt;
+      }
+      run += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
 }
@@ -280,8 +293,8 @@ size_t coarse_bitmap_bytes(const vsa_layout_t& L, int64_t bh) {
 static int build_csr(const vsa_layout_t& L, int64_t bh, int32_t* offs, int32_t* idx, int64_t top_k,
                      const uint32_t* bitmap, cudaStream_t st) {
   const int nc = int(L.nc), words = int((L.nc + 31) / 32);
-  bitmap_to_csr_kernel<<<unsigned(bh), 256, (nc + 1) * sizeof(int32_t), st>>>(nc, words, bitmap, offs, idx,
-                                                                              int64_t(nc) * top_k);
+  bitmap_to_csr_kernel<<<dim3(unsigned((nc + 7) / 8), unsigned(bh)), 256, 0, st>>>(nc, words, bitmap, offs, idx,
+                                                                                    int64_t(nc) * top_k);
   VSA_LAUNCH_CHECK("bitmap_to_csr_kernel");
 }
 
