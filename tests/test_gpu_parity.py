@@ -227,3 +227,36 @@ def test_host_pipeline_matches_resident_op(vsa):
         torch.cuda.synchronize()
         for a, b in zip(hout, ref):
             assert torch.equal(a, b.cpu()), f"chunks={chunks}"
+
+
+def test_fine_backward_skewed_transposed_map(vsa):
+    """Persistent dK/dV with the dynamic key-cube hand-out (2048 tasks over the SMs,
+    ring wrap-around, double-buffered accumulators, K/V reloads): a block map whose
+    transposed lists are very uneven (8 hot key cubes in every other row, many key
+    cubes selected by nobody) against the SIMT path on the same bf16 inputs, with and
+    without the dS workspace; and run-to-run bitwise determinism."""
+    g = torch.Generator(device="cuda").manual_seed(7)
+    L = vsa.TileLayout(16, 32, 32)  # nc = 256
+    B, H, d, k, nc = 1, 8, 128, 8, 256
+    rnd = lambda: (torch.randn((B, H, L.seq_len, d), generator=g, device="cuda")).bfloat16()
+    q, kk, v, do = rnd(), rnd(), rnd(), rnd()
+    gen = np.random.default_rng(8)
+    rows = []
+    for _ in range(B * H * nc):
+        hot = gen.choice(8, 4, replace=False) if gen.random() < 0.5 else np.array([], dtype=np.int64)
+        rest = gen.choice(np.arange(8 + 64, nc), k - len(hot), replace=False)  # cubes 8..71: never selected
+        rows.append(np.sort(np.concatenate([hot, rest])))
+    sel = torch.from_numpy(np.stack(rows).astype(np.int32)).view(B, H, nc, k).cuda()
+    res = vsa.fine_forward(L, q, kk, v, sel)
+    ref = vsa.fine_backward(L, q, kk, v, sel, do, res.row_lse, out=res.out, force_simt=True)
+    a = vsa.fine_backward(L, q, kk, v, sel, do, res.row_lse, out=res.out)
+    b = vsa.fine_backward(L, q, kk, v, sel, do, res.row_lse, out=res.out)
+    c = vsa.fine_backward(L, q, kk, v, sel, do, res.row_lse, out=res.out, workspace=False)
+    for got, r, n in zip(a, ref, ("dq", "dk", "dv")):
+        assert_close(host(got), host(r), torch.bfloat16, n)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    for got, r, n in zip(c, ref, ("dq", "dk", "dv")):
+        assert_close(host(got), host(r), torch.bfloat16, n + " (no workspace)")
+    dk = a[1].view(B, H, nc, 64, d)
+    assert (dk[:, :, 8:72] == 0).all()  # key cubes nobody selected
