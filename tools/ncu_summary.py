@@ -36,6 +36,11 @@ for r in rows[2:]:
         "dram_write_GB": val(r, "dram__bytes_write.sum"),
         "tensor_pipe_active_pct": val(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
         "bf16_mma_pct_of_peak": val(r, "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed"),
+        # SMEM data pipe: tensor-core operand reads + thread (LSU) shared loads / stores
+        "smem_tc_wavefronts_pct": val(r, "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+        "smem_lsu_wavefronts_pct": val(r, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+        "smem_bank_reads_pct": val(r, "l1tex__data_bank_reads.avg.pct_of_peak_sustained_elapsed"),
+        "smem_bank_writes_pct": val(r, "l1tex__data_bank_writes.avg.pct_of_peak_sustained_elapsed"),
         "sm_throughput_pct": val(r, "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
         "dram_throughput_pct": val(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
         "sm_clock_GHz": val(r, "sm__cycles_elapsed.avg.per_second"),
