@@ -311,6 +311,19 @@ def run_ours(args, rank, world, local_rank):
             traffic = tj.get(args.config, {}).get(dom)
         except Exception:
             traffic = None
+    # the binding resource of the fine kernels: the SM's shared-memory data pipe
+    # (tensor-core operand reads + thread shared stores), from the committed ncu summary
+    smem_pipe = None
+    npath = os.path.join(ROOT, "profiles", "ncu_r1d_kernels.json")
+    if os.path.exists(npath) and args.config == "wan13" and d == 128:
+        try:
+            with open(npath) as f:
+                ks = json.load(f)["kernels"]
+            smem_pipe = {k["kernel"].split("(")[0].split()[-1]: round(k["smem_tc_wavefronts_pct"] +
+                                                                      k["smem_lsu_wavefronts_pct"], 1)
+                         for k in ks if k.get("smem_tc_wavefronts_pct")}
+        except Exception:
+            smem_pipe = None
     bytes_tp = cfg["B"] * cfg["H"] * 3 * (S * d * 2 + L.seq_padded * d * 2 + nc * d * 4)
     stages = {}
     for s in STAGES:
@@ -345,7 +358,11 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(ach, 1), "peak": peaks["bf16_sust"],
                      "peak_kind": f"bf16_tflops_sustained ({peaks['src']})", "unit": "TFLOP/s",
                      "frac": round(ach / peaks["bf16_sust"], 4), "traffic": traffic,
-                     "algorithmic_flops_per_launch": fl[dom]},
+                     "algorithmic_flops_per_launch": fl[dom],
+                     "smem_pipe_busy_pct": smem_pipe,
+                     "note": "N=64 SS UMMAs are capped at 2/3 of the tensor peak by the 128 B/cycle SMEM "
+                             "operand port; smem_pipe_busy_pct = ncu TC + LSU shared wavefronts per kernel "
+                             "(profiles/ncu_r1d_kernels.json, DESIGN.md section 4)"},
         "stages": stages,
         "dense_baseline": dense,
         "gate_projection": gate,
