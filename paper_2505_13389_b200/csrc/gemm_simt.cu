@@ -142,24 +142,45 @@ __device__ __forceinline__ void gemm_f32_tile_pipe(const GemmArgs& g, int b, flo
   const float* Bm = g.B + b * g.sBb;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int nk = g.K / kGK;
-  auto load = [&](int stage, int t) {
-    const int k0 = t * kGK;
-    float* as = As + stage * kStageF;
-    float* bs = Bs + stage * kStageF;
-    if (AK) {
-      const int m = tid >> 2, kc = (tid & 3) * 4, gm = m0 + m;
-      cp_async16(as + m * kKF + kc, A + int64_t(min(gm, g.M - 1)) * g.sAm + k0 + kc, gm < g.M);
-    } else {
-      const int k = tid >> 4, mc = (tid & 15) * 4, gm = m0 + mc;
-      cp_async16(as + k * kMF + mc, A + int64_t(k0 + k) * g.sAk + min(gm, g.M - 4), gm < g.M);
-    }
-    if (BN) {
-      const int k = tid >> 4, nc = (tid & 15) * 4, gn = n0 + nc;
-      cp_async16(bs + k * kMF + nc, Bm + int64_t(k0 + k) * g.sBk + min(gn, g.N - 4), gn < g.N);
-    } else {
-      const int n = tid >> 2, kc = (tid & 3) * 4, gn = n0 + n;
-      cp_async16(bs + n * kKF + kc, Bm + int64_t(min(gn, g.N - 1)) * g.sBn + k0 + kc, gn < g.N);
-    }
+  // Per-thread copy descriptors, fixed for the whole K loop: one 16-byte chunk of A
+  // and one of B per slab; the source advances by a constant stride per slab (no
+  // per-slab address arithmetic or parameter loads in the main loop).
+  const float* pa;
+  const float* pb;
+  int64_t stepA, stepB;
+  int offA, offB;
+  bool va, vb;
+  if (AK) {
+    const int m = tid >> 2, kc = (tid & 3) * 4, gm = m0 + m;
+    va = gm < g.M;
+    pa = A + int64_t(min(gm, g.M - 1)) * g.sAm + kc;
+    stepA = kGK;
+    offA = m * kKF + kc;
+  } else {
+    const int k = tid >> 4, mc = (tid & 15) * 4, gm = m0 + mc;
+    va = gm < g.M;
+    pa = A + int64_t(k) * g.sAk + min(gm, g.M - 4);
+    stepA = int64_t(kGK) * g.sAk;
+    offA = k * kMF + mc;
+  }
+  if (BN) {
+    const int k = tid >> 4, nc = (tid & 15) * 4, gn = n0 + nc;
+    vb = gn < g.N;
+    pb = Bm + int64_t(k) * g.sBk + min(gn, g.N - 4);
+    stepB = int64_t(kGK) * g.sBk;
+    offB = k * kMF + nc;
+  } else {
+    const int n = tid >> 2, kc = (tid & 3) * 4, gn = n0 + n;
+    vb = gn < g.N;
+    pb = Bm + int64_t(min(gn, g.N - 1)) * g.sBn + kc;
+    stepB = kGK;
+    offB = n * kKF + kc;
+  }
+  auto load = [&](int stage) {  // the next slab in order; advances the sources
+    cp_async16(As + stage * kStageF + offA, pa, va);
+    cp_async16(Bs + stage * kStageF + offB, pb, vb);
+    pa += stepA;
+    pb += stepB;
   };
   float acc[4][4];
 #pragma unroll
@@ -168,14 +189,15 @@ __device__ __forceinline__ void gemm_f32_tile_pipe(const GemmArgs& g, int b, flo
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 #pragma unroll
   for (int s = 0; s < kPS - 1; ++s) {
-    if (s < nk) load(s, s);
+    if (s < nk) load(s);
     cp_async_commit();
   }
+  int cs = 0, ls = kPS - 1;  // stage computed / stage loaded next
   for (int t = 0; t < nk; ++t) {
     cp_async_wait<kPS - 2>();
     __syncthreads();
-    const float* as = As + (t % kPS) * kStageF;
-    const float* bs = Bs + (t % kPS) * kStageF;
+    const float* as = As + cs * kStageF;
+    const float* bs = Bs + cs * kStageF;
 #pragma unroll
     for (int kq = 0; kq < kGK; kq += 4) {
       float av[4][4], bv[4][4];  // [row / col][kk]
@@ -212,8 +234,10 @@ __device__ __forceinline__ void gemm_f32_tile_pipe(const GemmArgs& g, int b, flo
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(av[i][kk], bv[j][kk], acc[i][j]);
     }
-    if (t + kPS - 1 < nk) load((t + kPS - 1) % kPS, t + kPS - 1);
+    if (t + kPS - 1 < nk) load(ls);
     cp_async_commit();
+    cs = cs == kPS - 1 ? 0 : cs + 1;
+    ls = ls == kPS - 1 ? 0 : ls + 1;
   }
   cp_async_wait<0>();
   float* C = g.C + b * g.sCb;
