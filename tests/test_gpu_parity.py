@@ -260,3 +260,22 @@ def test_fine_backward_skewed_transposed_map(vsa):
         assert_close(host(got), host(r), torch.bfloat16, n + " (no workspace)")
     dk = a[1].view(B, H, nc, 64, d)
     assert (dk[:, :, 8:72] == 0).all()  # key cubes nobody selected
+
+
+@pytest.mark.parametrize("top_k", [1, 3, 15], ids=["k1", "k3", "k15"])
+def test_fine_odd_and_unit_k(vsa, top_k):
+    """Single-cube last pairs on the tcgen05 path (k = 1: every pair is a single cube;
+    odd k: one per row) in the forward, the transposed-map pairs of dK/dV and dQ."""
+    p = Problem(grid=(16, 16, 16), B=1, H=2, d=128, top_k=top_k, seed=57)
+    L = layout_of(vsa, p)
+    sel = orc.random_selection(p.B, p.H, L.num_cubes, p.top_k, orc.Rng(58))
+    q, k, v, do = (p.pad_tile(rounded(x, torch.bfloat16)) for x in (p.q, p.k, p.v, p.dout))
+    fo, _, flse = orc.fine_forward(p.olayout, q, k, v, sel)
+    fdq, fdk, fdv = orc.fine_backward(p.olayout, q, k, v, sel, do, flse)
+    dq_, dk_, dv_, do_ = (to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    dsel = to_dev(sel, torch.int32)
+    res = vsa.fine_forward(L, dq_, dk_, dv_, dsel)
+    assert_close(host(res.out), fo, torch.bfloat16, "fine out")
+    g = vsa.fine_backward(L, dq_, dk_, dv_, dsel, do_, res.row_lse, out=res.out)
+    for got, ref, n in zip(g, (fdq, fdk, fdv), ("dq", "dk", "dv")):
+        assert_close(host(got), ref, torch.bfloat16, n)
