@@ -38,9 +38,11 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
   const int tsr = blockIdx.y;
   const int64_t u = g / L.nc;
   const int c = int(g - u * L.nc);
-  const T* __restrict__ x = a.x[tsr];
-  T* __restrict__ xt = a.xt[tsr];
-  float* __restrict__ pooled = a.pooled[tsr];
+  // select without dynamic indexing of the parameter arrays (which would copy them to
+  // the local stack)
+  const T* __restrict__ x = tsr == 0 ? a.x[0] : tsr == 1 ? a.x[1] : a.x[2];
+  T* __restrict__ xt = tsr == 0 ? a.xt[0] : tsr == 1 ? a.xt[1] : a.xt[2];
+  float* __restrict__ pooled = tsr == 0 ? a.pooled[0] : tsr == 1 ? a.pooled[1] : a.pooled[2];
 
   const int plane = L.nh * L.nw;
   const int ci = c / plane, rem = c - ci * plane, cj = rem / L.nw, ck = rem - cj * L.nw;
@@ -50,6 +52,37 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
 #pragma unroll
   for (int i = 0; i < V; ++i) acc[i] = 0.f;
   const int64_t tile_base = u * L.seqp + int64_t(c) * L.cube;
+  if (L.cube % 8 == 0) {
+    // 8 tokens per batch, loads issued before use (memory-level parallelism); same
+    // per-channel order of the pooled sum (tile order)
+    const int hw = L.ch * L.cw;
+    for (int o0 = 0; o0 < L.cube; o0 += 8) {
+      uint4 raw[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int o = o0 + b;
+        const int oi = o / hw, r2 = o - oi * hw, oj = r2 / L.cw, ok = r2 - oj * L.cw;
+        const int t = t0 + oi, h = h0 + oj, w = w0 + ok;
+        const bool valid = in_tiled || (t < L.t && h < L.h && w < L.w);
+        const int64_t row = in_tiled ? tile_base + o : raster_row(L, u, (int64_t(t) * L.h + h) * L.w + w);
+        raw[b] = valid ? __ldg(reinterpret_cast<const uint4*>(x + row * d + ch * V)) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int o = o0 + b;
+        if (xt) *reinterpret_cast<uint4*>(xt + (tile_base + o) * d + ch * V) = raw[b];
+        float v[V];
+        load16(reinterpret_cast<const T*>(&raw[b]), v);
+        if (pool_mode == VSA_POOL_MEAN) {
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] = acc[i] + v[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] = (o == 0) ? v[i] : fmaxf_ordered(acc[i], v[i]);
+        }
+      }
+    }
+  } else {
   int o = 0;
   for (int oi = 0; oi < L.ct; ++oi)
     for (int oj = 0; oj < L.ch; ++oj)
@@ -74,6 +107,7 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
           for (int i = 0; i < V; ++i) acc[i] = (o == 0) ? v[i] : fmaxf_ordered(acc[i], v[i]);
         }
       }
+  }
   if (pooled) {
     if (pool_mode == VSA_POOL_MEAN) {
       const float inv = float(L.cube);
