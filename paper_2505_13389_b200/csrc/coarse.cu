@@ -78,9 +78,15 @@ __global__ void __launch_bounds__(128) coarse_softmax_topk_kernel(int64_t rows, 
   for (int j = lane; j < nc; j += 32) fv[j] = canon_expf(__fsub_rn(fv[j], m));
   __syncwarp();
   float sum = 0.f;
-  if (lane == 0) {
-#pragma unroll 8
-    for (int j = 0; j < nc; ++j) sum = __fadd_rn(sum, fv[j]);
+  if (lane == 0) {  // sequential in index order (the oracle's order), 16-byte loads
+    const int n4 = (nc & 3) == 0 ? nc >> 2 : 0;  // per-warp rows are 16-byte aligned iff nc % 4 == 0
+    const float4* f4 = reinterpret_cast<const float4*>(fv);
+#pragma unroll 4
+    for (int j = 0; j < n4; ++j) {
+      const float4 e = f4[j];
+      sum = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(sum, e.x), e.y), e.z), e.w);
+    }
+    for (int j = n4 * 4; j < nc; ++j) sum = __fadd_rn(sum, fv[j]);
   }
   sum = __shfl_sync(0xffffffffu, sum, 0);
   for (int j = lane; j < nc; j += 32) {

@@ -14,6 +14,7 @@ pytestmark = pytest.mark.gpu
 TINY = dict(grid=(8, 16, 16), B=1, H=2, d=64, top_k=4)           # BASELINE configs[0]
 PADDED = dict(grid=(9, 14, 22), B=2, H=2, d=64, top_k=6)          # non-divisible grid
 D128 = dict(grid=(16, 16, 16), B=1, H=2, d=128, top_k=8)
+ODD_NC = dict(grid=(12, 4, 20), B=1, H=3, d=64, top_k=5)         # nc = 15: odd row lengths everywhere
 DTYPES = [torch.float32, torch.bfloat16]
 
 
@@ -56,7 +57,7 @@ def test_flatten_index_matches_oracle(vsa):
         vsa.TileLayout(5, 4, 4, 2, 2, 2)
 
 
-@pytest.mark.parametrize("cfg", [TINY, PADDED, D128], ids=["tiny", "padded", "d128"])
+@pytest.mark.parametrize("cfg", [TINY, PADDED, D128, ODD_NC], ids=["tiny", "padded", "d128", "odd_nc"])
 def test_coarse_blockmap_bitexact(vsa, cfg):
     """fp32 coarse stage: probabilities, Oc and the Top-K block map bit-exact."""
     p = Problem(**cfg, seed=31)
