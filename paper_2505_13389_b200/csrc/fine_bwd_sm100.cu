@@ -105,29 +105,6 @@ __device__ __forceinline__ int64_t cube_out_row(const DevLayout& L, int64_t u, i
   return rr < 0 ? -1 : raster_row(L, u, rr);
 }
 
-// As write_rows, with the cube-level unpool term already in a D-float row (smem) and
-// the 64 output row indices precomputed (rows[r] < 0: pad token, dropped).
-template <int D>
-__device__ __forceinline__ void write_rows_x(const DevLayout& L, int64_t u, int cube, const float* st,
-                                             const float* xrow, const int64_t* rows, __nv_bfloat16* __restrict__ dst,
-                                             int tid, int nthr) {
-  constexpr int CH = D / 8;
-  const float inv = 1.0f / float(L.cube);
-  for (int task = tid; task < 64 * CH; task += nthr) {
-    const int r = task / CH, ch = task - r * CH;
-    float v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = st ? st[r * D + ch * 8 + i] : 0.f;
-    if (xrow) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] += xrow[ch * 8 + i] * inv;
-    }
-    const int64_t row = rows[r];
-    if (row < 0) continue;
-    store16(dst + row * D + ch * 8, v);
-  }
-}
-
 // Write a [64][D] fp32 staged tile as bf16 rows of cube `cube`, adding xc/64 (mean unpool).
 template <int D>
 __device__ __forceinline__ void write_rows(const DevLayout& L, int64_t u, int cube, const float* st,
