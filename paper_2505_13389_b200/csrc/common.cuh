@@ -86,6 +86,21 @@ __device__ __forceinline__ void load16(const __nv_bfloat16* p, float (&v)[8]) {
     v[2 * i] = f.x; v[2 * i + 1] = f.y;
   }
 }
+// Streaming (evict-first) variants for tensors touched once per step: their lines
+// should not displace the tiles the fine kernels re-read from L2.
+__device__ __forceinline__ void load16_cs(const __nv_bfloat16* p, float (&v)[8]) {
+  uint4 x = __ldcs(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x; v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void load16_cs(const float* p, float (&v)[4]) {
+  float4 x = __ldcs(reinterpret_cast<const float4*>(p));
+  v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
 __device__ __forceinline__ void store16(float* p, const float (&v)[4]) {
   *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
 }
@@ -95,6 +110,16 @@ __device__ __forceinline__ void store16(__nv_bfloat16* p, const float (&v)[8]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
   *reinterpret_cast<uint4*>(p) = x;
+}
+__device__ __forceinline__ void store16_cs(float* p, const float (&v)[4]) {
+  __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+}
+__device__ __forceinline__ void store16_cs(__nv_bfloat16* p, const float (&v)[8]) {
+  uint4 x;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  __stcs(reinterpret_cast<uint4*>(p), x);
 }
 
 // std::max(a, b) semantics of the oracle: (a < b) ? b : a

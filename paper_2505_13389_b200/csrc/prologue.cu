@@ -51,11 +51,11 @@ __global__ void __launch_bounds__(128) prologue_kernel(DevLayout L, int64_t bh, 
     float part = 0.f;
     if (valid) {
       float g_o[V], g_c[V], g_f[V], f_o[V], r_f[V];
-      load16(dout + srow * d + ch * V, g_o);
-      load16(gc + srow * d + ch * V, g_c);
+      load16_cs(dout + srow * d + ch * V, g_o);
+      load16_cs(gc + srow * d + ch * V, g_c);
       load16(of + trow * d + ch * V, f_o);
       if (!adaptation) {
-        load16(gf + srow * d + ch * V, g_f);
+        load16_cs(gf + srow * d + ch * V, g_f);
       } else {
 #pragma unroll
         for (int i = 0; i < V; ++i) g_f[i] = 1.f;
@@ -74,13 +74,13 @@ __global__ void __launch_bounds__(128) prologue_kernel(DevLayout L, int64_t bh, 
         float t[V];
 #pragma unroll
         for (int i = 0; i < V; ++i) t[i] = __fmul_rn(g_o[i], ocv[i]);
-        store16(dgc + srow * d + ch * V, t);
+        store16_cs(dgc + srow * d + ch * V, t);
       }
       if (dgf) {
         float t[V];
 #pragma unroll
         for (int i = 0; i < V; ++i) t[i] = adaptation ? 0.f : __fmul_rn(g_o[i], f_o[i]);
-        store16(dgf + srow * d + ch * V, t);
+        store16_cs(dgf + srow * d + ch * V, t);
       }
     } else if (active) {
       float z[V];

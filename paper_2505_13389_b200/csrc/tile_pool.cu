@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
         const int t = t0 + oi, h = h0 + oj, w = w0 + ok;
         const bool valid = in_tiled || (t < L.t && h < L.h && w < L.w);
         const int64_t row = in_tiled ? tile_base + o : raster_row(L, u, (int64_t(t) * L.h + h) * L.w + w);
-        raw[b] = valid ? __ldg(reinterpret_cast<const uint4*>(x + row * d + ch * V)) : make_uint4(0, 0, 0, 0);
+        raw[b] = valid ? __ldcs(reinterpret_cast<const uint4*>(x + row * d + ch * V)) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
