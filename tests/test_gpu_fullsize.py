@@ -75,3 +75,27 @@ def test_fullsize_backward_linear_in_dout(vsa, problem):
     for a, b, ab, n in zip(ga, gb, gab, ("dq", "dk", "dv", "dgc", "dgf")):
         # bf16 rounding of dO1 + dO2 and of each result bounds the deviation
         assert_close(host(ab), host(a + b), torch.bfloat16, n)
+
+
+def test_coarse_large_bitexact(vsa):
+    """The coarse stage at a size with many GEMM tiles per launch (6 heads, nc = 576
+    with edge tiles): probabilities, block map and Oc bit-exact with the oracle,
+    coarse gradients equal to the oracle's."""
+    import oracle as orc
+
+    L = vsa.TileLayout(16, 48, 48)
+    OL = orc.TileLayout(16, 48, 48, 4, 4, 4)
+    B, H, d, k = 1, 6, 128, 72
+    rng = orc.Rng(36)
+    q, kk, v, doc = (orc.randn(rng, B, H, L.seq_len, d, np.float32) for _ in range(4))
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    art = vsa.coarse_forward_select(L, dev(q), dev(kk), dev(v), k)
+    ref = orc.coarse_forward_select(OL, q, kk, v, k)
+    assert L.num_cubes == 576
+    np.testing.assert_array_equal(art.ac.cpu().numpy(), ref.ac)
+    np.testing.assert_array_equal(art.sel.cpu().numpy(), ref.sel)
+    np.testing.assert_array_equal(art.oc_cube.cpu().numpy(), ref.oc_cube)
+    got = vsa.coarse_backward(art, L, dev(doc), dev(q), dev(kk), dev(v))
+    exp = orc.coarse_backward(ref, OL, doc, q, kk, v)
+    for g, e, n in zip(got, exp, ("dq", "dk", "dv")):
+        np.testing.assert_allclose(g.cpu().numpy(), e, rtol=1e-5, atol=1e-6, err_msg=n)
