@@ -15,6 +15,7 @@ TINY = dict(grid=(8, 16, 16), B=1, H=2, d=64, top_k=4)           # BASELINE conf
 PADDED = dict(grid=(9, 14, 22), B=2, H=2, d=64, top_k=6)          # non-divisible grid
 D128 = dict(grid=(16, 16, 16), B=1, H=2, d=128, top_k=8)
 ODD_NC = dict(grid=(12, 4, 20), B=1, H=3, d=64, top_k=5)         # nc = 15: odd row lengths everywhere
+PADDED128 = dict(grid=(9, 14, 22), B=2, H=2, d=128, top_k=7)      # batch 2, padded, d = 128, odd k
 DTYPES = [torch.float32, torch.bfloat16]
 
 
@@ -98,7 +99,7 @@ def test_topk_ties_lower_index(vsa):
     np.testing.assert_array_equal(art.sel.cpu().numpy()[0, 0], ref_rows)
 
 
-@pytest.mark.parametrize("cfg", [TINY, PADDED, D128], ids=["tiny", "padded", "d128"])
+@pytest.mark.parametrize("cfg", [TINY, PADDED, D128, PADDED128], ids=["tiny", "padded", "d128", "padded128"])
 @pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
 def test_fine_forward_backward(vsa, cfg, dtype):
     """fine_forward / fine_backward on tile-ordered inputs with a random block map."""
@@ -141,7 +142,7 @@ def test_dense_baseline_is_dense_attention(vsa, dtype):
     assert_close(host(res.out), dense, dtype, "dense")
 
 
-@pytest.mark.parametrize("cfg", [TINY, PADDED, D128], ids=["tiny", "padded", "d128"])
+@pytest.mark.parametrize("cfg", [TINY, PADDED, D128, PADDED128], ids=["tiny", "padded", "d128", "padded128"])
 @pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
 def test_vsa_op_end_to_end(vsa, cfg, dtype):
     """The full operator, raster in / raster out: forward, block map, backward incl. gate grads."""
