@@ -67,13 +67,13 @@ class Problem:
     def untile_crop(self, xt):
         return orc.crop_raster(orc.untile(self.olayout, xt), self.grid, self.padded)
 
-    def oracle(self, dtype, sel_override=None, backward=True, heads=None):
+    def oracle(self, dtype, sel_override=None, backward=True, heads=None, pool=None):
         """Reference semantics on the zero-padded problem."""
         hs = slice(None) if heads is None else heads
         r = lambda a: rounded(a[:, hs], dtype)
         q, k, v, gc, gf, do = (self.pad_tile(r(x)) for x in (self.q, self.k, self.v, self.gc, self.gf, self.dout))
         L = self.olayout
-        art = orc.coarse_forward_select(L, q, k, v, self.top_k)
+        art = orc.coarse_forward_select(L, q, k, v, self.top_k, *(() if pool is None else (pool,)))
         sel = art.sel if sel_override is None else np.ascontiguousarray(sel_override[:, hs])
         fo, _, lse = orc.fine_forward(L, q, k, v, sel)
         out = art.oc * gc + fo * gf

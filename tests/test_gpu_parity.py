@@ -282,3 +282,18 @@ def test_fine_odd_and_unit_k(vsa, top_k):
     g = vsa.fine_backward(L, dq_, dk_, dv_, dsel, do_, res.row_lse, out=res.out)
     for got, ref, n in zip(g, (fdq, fdk, fdv), ("dq", "dk", "dv")):
         assert_close(host(got), ref, torch.bfloat16, n)
+
+
+@pytest.mark.parametrize("cfg", [TINY, PADDED128], ids=["tiny", "padded128"])
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
+def test_vsa_op_max_pool(vsa, cfg, dtype):
+    """PoolMode::kMax end to end (coarse.hpp:47-65 forward, 172-176 first-argmax unpool)."""
+    p = Problem(**cfg, seed=73)
+    L = layout_of(vsa, p)
+    op = vsa.VsaOp(L, p.B, p.H, p.d, p.top_k, dtype=dtype, pool=vsa.POOL_MAX)
+    out = op.forward(*[to_dev(x, dtype) for x in (p.q, p.k, p.v, p.gc, p.gf)])
+    ref = p.oracle(dtype, pool=orc.KMAX)
+    np.testing.assert_array_equal(op.sel.cpu().numpy(), ref["sel"])
+    assert_close(host(out), ref["out"], dtype, "out")
+    for got, n in zip(op.backward(to_dev(p.dout, dtype)), ("dq", "dk", "dv", "dgc", "dgf")):
+        assert_close(host(got), ref[n], dtype, n)
