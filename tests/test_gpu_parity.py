@@ -297,3 +297,29 @@ def test_vsa_op_max_pool(vsa, cfg, dtype):
     assert_close(host(out), ref["out"], dtype, "out")
     for got, n in zip(op.backward(to_dev(p.dout, dtype)), ("dq", "dk", "dv", "dgc", "dgf")):
         assert_close(host(got), ref[n], dtype, n)
+
+
+SWEEP_CUBES = [(4, 4, 4), (2, 4, 8), (1, 8, 8), (4, 2, 8), (8, 8, 1)]
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_randomized_sweep_tcgen05(vsa, case):
+    """Seeded sweep in the spirit of the reference's verify suite (verify.hpp:99-134):
+    random grids (padded or not), 64-token cube shapes of every orientation, batch,
+    heads, d in {64, 128} and k in [1, nc] through the full bf16 operator vs the oracle."""
+    g = np.random.default_rng(1000 + case)
+    cube = SWEEP_CUBES[case % len(SWEEP_CUBES)]
+    grid = tuple(int(c * g.integers(1, 4) + (g.integers(0, c) if case % 3 == 0 else 0)) for c in cube)
+    grid = tuple(max(x, 1) for x in grid)
+    B, H, d = int(g.integers(1, 3)), int(g.integers(1, 4)), int(g.choice([64, 128]))
+    nc = int(np.prod([(e + c - 1) // c for e, c in zip(grid, cube)]))
+    p = Problem(grid=grid, B=B, H=H, d=d, top_k=int(g.integers(1, nc + 1)), seed=90 + case, cube=cube)
+    L = layout_of(vsa, p)
+    assert L.num_cubes == nc
+    op = vsa.VsaOp(L, p.B, p.H, p.d, p.top_k)
+    out = op.forward(*[to_dev(x, torch.bfloat16) for x in (p.q, p.k, p.v, p.gc, p.gf)])
+    ref = p.oracle(torch.bfloat16)
+    np.testing.assert_array_equal(op.sel.cpu().numpy(), ref["sel"])
+    assert_close(host(out), ref["out"], torch.bfloat16, "out")
+    for got, n in zip(op.backward(to_dev(p.dout, torch.bfloat16)), ("dq", "dk", "dv", "dgc", "dgf")):
+        assert_close(host(got), ref[n], torch.bfloat16, n)
