@@ -294,6 +294,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
 
   if (warp == 9) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kKVRegCtl));
+    // (Measured alternatives: st.global of dS from the compute warps,
+    // even with a coalesced tile layout, and a second dS buffer both ran slower.)
     // dS tile store: TMA-store the bf16 [64 q][64 keys] tiles of every pair for the dQ
     // GEMM — tile (qcube, t) at rows ((u*nc + qcube)*k + t)*64, t = position of kc in
     // sel[qcube] — then release the buffer to the compute warps.
