@@ -52,13 +52,18 @@ CONFIGS = {
 STAGES = ["tile_pool", "coarse_fwd", "fine_fwd", "prologue", "coarse_bwd", "fine_bwd"]
 
 
+def metric_name(cfg):
+    """The one metric string both arms print (the driver pairs the lines on it)."""
+    return f"VSA fwd+bwd effective TFLOPS (algorithmic FLOPs / device time), {cfg['workload']}"
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
         return dict(hbm=p["hbm_gbs"], bf16=p["bf16_tflops"], bf16_sust=p["bf16_tflops_sustained"], src="measured")
     except Exception:
-        return dict(hbm=6650.0, bf16=1590.0, bf16_sust=1400.0, src="fallback")
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sust=1400.0, src="fallback (B200_PROFILING.md)")
 
 
 def flops(cfg, nc, top_k, d, cube=64):
@@ -145,13 +150,19 @@ class ClockSampler:
                 "samples": len(s), "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
-def make_inputs(cfg, S, dtype, device, seed=0):
+def make_inputs(cfg, S, dtype, device, u0, u1):
+    """q, k, v, gc, gf, dO of (b,h) units [u0, u1) as [1, u1-u0, S, d]; each unit drawn from
+    its own seeded generator, so a unit's data does not depend on the partition."""
     import torch
 
+    n, d = u1 - u0, cfg["d"]
+    xs = [torch.empty((1, n, S, d), dtype=dtype, device=device) for _ in range(6)]
     g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    shape = (cfg["B"], cfg["H"], S, cfg["d"])
-    return [torch.randn(shape, generator=g, device=device, dtype=torch.float32).to(dtype) for _ in range(6)]
+    for j, u in enumerate(range(u0, u1)):
+        g.manual_seed(1234 + u)
+        for x in xs:
+            x[0, j].copy_(torch.randn((S, d), generator=g, device=device, dtype=torch.float32))
+    return xs
 
 
 def run_ours(args, rank, world, local_rank):
@@ -169,11 +180,21 @@ def run_ours(args, rank, world, local_rank):
     fl = flops(cfg, nc, K, d)
     peaks = load_peaks()
 
-    op = vsa.VsaOp(L, cfg["B"], cfg["H"], d, K, dtype=dtype)
-    q, k, v, gc, gf, do = make_inputs(cfg, S, dtype, dev, seed=1234 + rank)
+    # batch x head partition of the ONE problem: this rank's contiguous unit
+    # range, no data-path collective (strong scaling; paper_2505_13389_b200/partition.py)
+    from paper_2505_13389_b200.partition import partition_units
+
+    units = cfg["B"] * cfg["H"]
+    parts = partition_units(units, world)
+    u0, u1 = parts[rank]
+    n = u1 - u0
+    op = vsa.VsaOp(L, 1, n, d, K, dtype=dtype) if n else None
+    q, k, v, gc, gf, do = make_inputs(cfg, S, dtype, dev, u0, u1)
     outs = [torch.empty_like(q) for _ in range(6)]
 
     def step():
+        if op is None:
+            return
         op.forward(q, k, v, gc, gf, out=outs[0], check_inputs=False)
         op.backward(do, *outs[1:], check_inputs=False)
 
@@ -204,28 +225,28 @@ def run_ours(args, rank, world, local_rank):
         barrier()
     launches = lib.vsa_kernel_launches() - n0
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    value = world * fl["total"] / (ms * 1e-3) / 1e12
+    value = fl["total"] / (ms * 1e-3) / 1e12  # the whole problem over the slowest rank
 
-    # per-stage breakdown (events between stages on the launch stream)
-    stage_ms = {s: 0.0 for s in STAGES}
-    nrep = max(2, min(args.steps, 5))
-    for _ in range(nrep):
-        op.trace = []
-        step()
-        torch.cuda.synchronize()
-        tr = op.trace
-        for (_, a), (name, b) in zip(tr[:-1], tr[1:]):
-            if name in stage_ms:
-                stage_ms[name] += a.elapsed_time(b) / nrep
-    op.trace = None
+    # per-stage breakdown: CUDA events recorded by the native operator between its stages
+    # on the launch stream, over back-to-back steps (no host gaps), one sync at the end
+    nrep = max(3, min(args.steps, 10))
+    stage_ms = {s_: 0.0 for s_ in STAGES}
+    if op is not None:
+        op.timing(True)
+        for _ in range(nrep):
+            step()
+        stage_ms = op.stage_ms()
+        op.timing(False)
 
     # dense baseline: the same kernels with top-k = all cubes
     dense = None
     if not args.no_dense:
-        opd = vsa.VsaOp(L, cfg["B"], cfg["H"], d, nc, dtype=dtype)
+        opd = vsa.VsaOp(L, 1, n, d, nc, dtype=dtype) if n else None
         fld = flops(cfg, nc, nc, d)
 
         def dstep():
+            if opd is None:
+                return
             opd.forward(q, k, v, gc, gf, out=outs[0], check_inputs=False)
             opd.backward(do, *outs[1:], check_inputs=False)
 
@@ -246,22 +267,23 @@ def run_ours(args, rank, world, local_rank):
     # gate projection (the rest of vsa_forward/vsa_backward): tcgen05 GEMMs
     # z = hidden.Wg (+bias, sigmoid, split) and dhidden / dWg / dbias, model_dim = H*d
     gate = None
-    if cfg["B"] * cfg["H"] * cfg["d"] % 256 == 0 and (cfg["H"] * cfg["d"]) % 256 == 0:
+    if world == 1 and cfg["B"] * cfg["H"] * cfg["d"] % 256 == 0 and (cfg["H"] * cfg["d"]) % 256 == 0:
         md = cfg["H"] * cfg["d"]
         hid = torch.randn((cfg["B"], 1, S, md), device=dev).to(dtype)
         wg = (torch.randn((md, 2 * cfg["H"] * d), device=dev) / md ** 0.5).to(dtype)
         gp = vsa.VsaParams(wg, torch.zeros(2 * cfg["H"] * d, device=dev), K, activation=1)
         gcg, gfg = vsa.gates_from_hidden(hid, gp, cfg["H"], d, layout=L)
+        qg, kg = q.view(gcg.shape), k.view(gcg.shape)  # stand-in upstream gate gradients
         g0, g1, g2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         for _ in range(2):
             vsa.gates_from_hidden(hid, gp, cfg["H"], d, layout=L)
-            vsa.gate_backward(hid, gp, gcg, gfg, q, k, layout=L)
+            vsa.gate_backward(hid, gp, gcg, gfg, qg, kg, layout=L)
         g0.record(st)
         for _ in range(5):
             vsa.gates_from_hidden(hid, gp, cfg["H"], d, layout=L)
         g1.record(st)
         for _ in range(5):
-            vsa.gate_backward(hid, gp, gcg, gfg, q, k, layout=L)
+            vsa.gate_backward(hid, gp, gcg, gfg, qg, kg, layout=L)
         g2.record(st)
         torch.cuda.synchronize()
         gfl = 2 * cfg["B"] * S * md * 2 * cfg["H"] * d
@@ -269,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
         gate = {"model_dim": md, "fwd_ms": round(tf, 4), "fwd_tflops": round(gfl / tf / 1e9, 1),
                 "bwd_ms": round(tb, 4), "bwd_tflops": round(2 * gfl / tb / 1e9, 1),
                 "note": "not in value: the BASELINE metric is the attention op; gates are inputs there"}
-        del hid, wg, gcg, gfg
+        del hid, wg, gcg, gfg, qg, kg
 
     # e2e through the public API with pinned host buffers: VsaHostPipeline overlaps the
     # H2D of unit-group i+1 and the D2H of group i-1 with the kernels of group i
@@ -277,10 +299,11 @@ def run_ours(args, rank, world, local_rank):
     hout = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
     del op  # free the resident-input operator's buffers before building the pipeline
     torch.cuda.empty_cache()
-    pipe = vsa.VsaHostPipeline(L, cfg["B"], cfg["H"], d, K, chunks=args.e2e_chunks, dtype=dtype)
+    pipe = vsa.VsaHostPipeline(L, 1, n, d, K, chunks=min(args.e2e_chunks, n), dtype=dtype) if n else None
 
     def e2e_step():
-        pipe.run(hin, hout)
+        if pipe is not None:
+            pipe.run(hin, hout)
 
     e2e_step()
     barrier()
@@ -295,13 +318,18 @@ def run_ours(args, rank, world, local_rank):
     ems = max_over_ranks(e2.elapsed_time(e3) / ne)
     h2d = sum(t.numel() * t.element_size() for t in hin)
     d2h = sum(t.numel() * t.element_size() for t in hout)
+    if world > 1:  # whole-job bytes: every rank copies its own units
+        t = torch.tensor([h2d, d2h], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        h2d, d2h = int(t[0].item()), int(t[1].item())
 
     if rank != 0:
         return None
 
-    # roofline of the dominant kernel
+    # roofline of the dominant kernel (rank 0's share of the work: n units)
+    fl_r = flops(dict(B=1, H=max(n, 1)), nc, K, d)
     dom = max(("fine_fwd", "fine_bwd"), key=lambda s: stage_ms[s])
-    ach = fl[dom] / (stage_ms[dom] * 1e-3) / 1e12
+    ach = fl_r[dom] / (max(stage_ms[dom], 1e-9) * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -324,17 +352,17 @@ def run_ours(args, rank, world, local_rank):
                          for k in ks if k.get("smem_tc_wavefronts_pct")}
         except Exception:
             smem_pipe = None
-    bytes_tp = cfg["B"] * cfg["H"] * 3 * (S * d * 2 + L.seq_padded * d * 2 + nc * d * 4)
+    bytes_tp = n * 3 * (S * d * 2 + L.seq_padded * d * 2 + nc * d * 4)
     stages = {}
     for s in STAGES:
         e = {"ms": round(stage_ms[s], 4)}
         if s in ("fine_fwd", "fine_bwd", "coarse_fwd", "coarse_bwd") and stage_ms[s] > 0:
-            e["tflops"] = round(fl[s] / (stage_ms[s] * 1e-3) / 1e12, 1)
+            e["tflops"] = round(fl_r[s] / (stage_ms[s] * 1e-3) / 1e12, 1)
         if s == "tile_pool" and stage_ms[s] > 0:
             e["gbs"] = round(bytes_tp / (stage_ms[s] * 1e-3) / 1e9, 1)
         stages[s] = e
     line = {
-        "metric": f"VSA fwd+bwd effective TFLOPS (algorithmic FLOPs / device time), {cfg['workload']}",
+        "metric": metric_name(cfg),
         "value": round(value, 2),
         "unit": "TFLOP/s",
         "n_gpus": world,
@@ -342,23 +370,27 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": round(ms, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic (torch.randn, seeded per rank)",
+        "data": "synthetic (torch.randn, seeded per (b,h) unit)",
         "config": {
             "workload": cfg["workload"], "B": cfg["B"], "H": cfg["H"], "head_dim": d, "grid": list(cfg["grid"]),
             "grid_padded": list(L.padded), "cube": [4, 4, 4], "num_cubes": nc, "top_k": K,
-            "sparsity": round(1 - K / nc, 4), "global_batch": cfg["B"] * world, "seq_len": S,
-            "parallelism": f"dp{world} (batch x head partition, no collective)",
+            "sparsity": round(1 - K / nc, 4), "global_batch": cfg["B"], "seq_len": S,
+            "parallelism": f"bh{world}: batch x head partition of one problem, "
+                           f"{min(b - a for a, b in parts)}-{max(b - a for a, b in parts)} of {units} (b,h) units "
+                           f"per GPU, no collective",
             "l2": "inputs larger than L2 (6 x {:.0f} MB bf16 per step)".format(q.numel() * 2 / 1e6),
             "flops_per_step": fl["total"],
         },
-        "frac_of_peak": round(value / world / peaks["bf16_sust"], 4),
-        "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(ach, 1), "peak": peaks["bf16_sust"],
-                     "peak_kind": f"bf16_tflops_sustained ({peaks['src']})", "unit": "TFLOP/s",
-                     "frac": round(ach / peaks["bf16_sust"], 4), "traffic": traffic,
-                     "algorithmic_flops_per_launch": fl[dom],
+        "frac_of_peak": round(value / world / peaks["bf16"], 4),
+        "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(ach, 1), "peak": peaks["bf16"],
+                     "peak_kind": f"bf16_tflops burst ({peaks['src']}; the kernel is a ms-long launch timed "
+                                  f"inside a sub-second loop)", "unit": "TFLOP/s",
+                     "frac": round(ach / peaks["bf16"], 4), "frac_of_sustained": round(ach / peaks["bf16_sust"], 4),
+                     "traffic": traffic,
+                     "algorithmic_flops_per_launch": fl_r[dom],
                      "smem_pipe_busy_pct": smem_pipe,
                      "note": "N=64 SS UMMAs are capped at 2/3 of the tensor peak by the 128 B/cycle SMEM "
                              "operand port; smem_pipe_busy_pct = ncu TC + LSU shared wavefronts per kernel "
@@ -366,13 +398,13 @@ def run_ours(args, rank, world, local_rank):
         "stages": stages,
         "dense_baseline": dense,
         "gate_projection": gate,
-        "e2e": {"value": round(world * fl["total"] / (ems * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+        "e2e": {"value": round(fl["total"] / (ems * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                 "ms_per_step": round(ems, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(cfg, 1)
+        line["cpu_baseline"] = cpu_baseline(cfg, 3, warmup=1)
     return line
 
 
@@ -431,17 +463,12 @@ def run_sp(args, rank, world, local_rank):
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     value = fl["total"] / (ms * 1e-3) / 1e12
 
-    stage_ms = {s: 0.0 for s in STAGES}
-    nrep = max(2, min(args.steps, 3))
+    nrep = max(3, min(args.steps, 10))
+    u.op.timing(True)
     for _ in range(nrep):
-        u.op.trace = []
         step(shards)
-        torch.cuda.synchronize()
-        tr = u.op.trace
-        for (_, a), (name, b) in zip(tr[:-1], tr[1:]):
-            if name in stage_ms:
-                stage_ms[name] += a.elapsed_time(b) / nrep
-    u.op.trace = None
+    stage_ms = u.op.stage_ms()
+    u.op.timing(False)
 
     # e2e: pinned host shards in, the six results out, every step
     hin = [t.cpu().pin_memory() for t in shards]
@@ -473,7 +500,7 @@ def run_sp(args, rank, world, local_rank):
         if stage_ms[s] > 0:
             stages[s]["tflops"] = round(fl_rank[s] / (stage_ms[s] * 1e-3) / 1e12, 1)
     return {
-        "metric": "VSA fwd+bwd effective TFLOPS (algorithmic FLOPs / device time), Wan2.1-14B layer",
+        "metric": metric_name(cfg),
         "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (torch.randn, seeded per rank)",
@@ -482,10 +509,10 @@ def run_sp(args, rank, world, local_rank):
                    "sparsity": round(1 - K / nc, 4), "global_batch": B, "seq_len": S,
                    "parallelism": f"sp{P} (Ulysses all-to-all over NCCL, {H // P} heads per GPU)",
                    "l2": "inputs larger than L2", "flops_per_step": fl["total"]},
-        "frac_of_peak": round(value / world / peaks["bf16_sust"], 4),
-        "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(ach, 1), "peak": peaks["bf16_sust"],
-                     "peak_kind": f"bf16_tflops_sustained ({peaks['src']})", "unit": "TFLOP/s",
-                     "frac": round(ach / peaks["bf16_sust"], 4), "traffic": None,
+        "frac_of_peak": round(value / world / peaks["bf16"], 4),
+        "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(ach, 1), "peak": peaks["bf16"],
+                     "peak_kind": f"bf16_tflops burst ({peaks['src']})", "unit": "TFLOP/s",
+                     "frac": round(ach / peaks["bf16"], 4), "traffic": None,
                      "algorithmic_flops_per_launch": fl_rank[dom]},
         "stages": stages,
         "e2e": {"value": round(fl["total"] / (ems * 1e-3) / 1e12, 3), "unit": "TFLOP/s", "ms_per_step": round(ems, 3),
@@ -495,9 +522,9 @@ def run_sp(args, rank, world, local_rank):
     }
 
 
-def cpu_baseline(cfg, reps):
-    """The oracle (CPU restatement of the reference) on ONE (b,h) head of the
-    workload: coarse fwd + fine fwd + fine bwd + coarse bwd, all host threads."""
+def _oracle_head(cfg, seed):
+    """One (b,h) head of the workload for the CPU restatement: tile-ordered padded q, k, v,
+    dO drawn like the reference (mt19937_64, vsa_cli.cpp:227-230)."""
     import numpy as np
 
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -506,51 +533,70 @@ def cpu_baseline(cfg, reps):
     T, X, Y = cfg["grid"]
     Tp, Xp, Yp = orc.padded_extents(T, X, Y, 4, 4, 4)
     L = orc.TileLayout(Tp, Xp, Yp, 4, 4, 4)
-    d, K = cfg["d"], cfg["top_k"]
-    rng = orc.Rng(0)
-    q, k, v, do = (orc.randn(rng, 1, 1, L.seq_len, d, np.float32) for _ in range(4))
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        art = orc.coarse_forward_select(L, q, k, v, K)
-        _, _, lse = orc.fine_forward(L, q, k, v, art.sel)
-        orc.fine_backward(L, q, k, v, art.sel, do, lse)
-        orc.coarse_backward(art, L, do, q, k, v)
-        times.append(time.perf_counter() - t0)
-    t = sorted(times)[len(times) // 2]
-    fl = flops(dict(B=1, H=1), L.num_cubes, K, d)["total"]
+    rng = orc.Rng(seed)
+    q, k, v, do = (orc.randn(rng, 1, 1, L.seq_len, cfg["d"], np.float32) for _ in range(4))
+    return orc, L, (q, k, v, do)
+
+
+def _oracle_step(orc, L, x, K):
+    """coarse_forward_select + fine_forward + fine_backward + coarse_backward of one head
+    (the reference's vsa fwd + bwd attention work; vsa_cli.cpp:232-256 times the forward)."""
+    q, k, v, do = x
+    t0 = time.perf_counter()
+    art = orc.coarse_forward_select(L, q, k, v, K)
+    _, _, lse = orc.fine_forward(L, q, k, v, art.sel)
+    orc.fine_backward(L, q, k, v, art.sel, do, lse)
+    orc.coarse_backward(art, L, do, q, k, v)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, reps, warmup=1):
+    """The oracle (CPU restatement of the reference) on ONE (b,h) head of the workload:
+    coarse fwd + fine fwd + fine bwd + coarse bwd, all host threads; `warmup` untimed
+    runs, then the median of `reps` (the reference bench protocol, vsa_cli.cpp:232-256)."""
+    orc, L, x = _oracle_head(cfg, 0)
+    for _ in range(warmup):
+        _oracle_step(orc, L, x, cfg["top_k"])
+    times = sorted(_oracle_step(orc, L, x, cfg["top_k"]) for _ in range(reps))
+    t = times[len(times) // 2]
+    fl = flops(dict(B=1, H=1), L.num_cubes, cfg["top_k"], cfg["d"])["total"]
     return {"value": round(fl / t / 1e12, 5), "unit": "TFLOP/s", "cores": orc.max_threads(), "kind": "port",
             "sample": f"one (b,h) head of {cfg['workload']} (1/{cfg['B'] * cfg['H']} of a step), "
-                      f"coarse+fine fwd+bwd, {t:.2f} s median of {reps}", "seconds": round(t, 3)}
+                      f"coarse+fine fwd+bwd, median of {reps} after {warmup} warm-up: {t:.2f} s",
+            "seconds": round(t, 3)}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm on the host cores (the oracle
-    port; the Eigen reference cannot be compiled here), same metric/config."""
+    """--impl reference: the reference algorithm on the host cores (the oracle port; the
+    Eigen reference cannot be compiled here), same metric, unit and config as our arm.
+    Each step is a bounded sample of the workload: one (b,h) head's fwd + bwd (1/(B*H)
+    of the layer); `steps` samples are timed after `warmup` untimed ones, and ms_per_step
+    is the time of one such sample (what was actually timed)."""
     if rank != 0:
         return None
     cfg = CONFIGS[args.config]
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as orc
-
+    orc, L, x = _oracle_head(cfg, 0)
     orc.set_num_threads(os.cpu_count() or 1)
-    for _ in range(min(args.warmup, 1)):
-        cpu_baseline(cfg, 1)
-    cb = cpu_baseline(cfg, max(1, min(args.steps, 3)))
-    # one step of the full workload = B*H heads
-    heads = cfg["B"] * cfg["H"]
-    ms = cb["seconds"] * heads * 1e3
+    K = cfg["top_k"]
+    for _ in range(args.warmup):
+        _oracle_step(orc, L, x, K)
+    times = [_oracle_step(orc, L, x, K) for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    fl = flops(dict(B=1, H=1), L.num_cubes, K, cfg["d"])["total"]
+    value = fl / t / 1e12
+    sample = (f"one (b,h) head of {cfg['workload']} per step (1/{cfg['B'] * cfg['H']} of the layer): coarse+fine "
+              f"fwd+bwd, {args.steps} timed after {args.warmup} warm-up, mean {t:.3f} s")
     return {
-        "metric": "VSA fwd+bwd effective TFLOPS (algorithmic FLOPs / device time), Wan2.1-1.3B layer",
-        "impl": "reference", "value": cb["value"], "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (mt19937_64 randn)",
+        "metric": metric_name(cfg),
+        "impl": "reference", "value": round(value, 5), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (mt19937_64 randn, the reference's draws)",
         "config": {"workload": cfg["workload"], "B": cfg["B"], "H": cfg["H"], "head_dim": cfg["d"],
-                   "grid": list(cfg["grid"]), "top_k": cfg["top_k"],
-                   "note": "each step is a bounded sample: one (b,h) head; ms_per_step extrapolated x B*H"},
-        "cpu_baseline": {"value": cb["value"], "unit": "TFLOP/s", "cores": cb["cores"], "kind": "port",
-                         "sample": cb["sample"]},
-        "e2e": {"value": cb["value"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "grid": list(cfg["grid"]), "top_k": K, "num_cubes": L.num_cubes,
+                   "sample": "one (b,h) head per step; value = that head's algorithmic FLOPs / its time"},
+        "cpu_baseline": {"value": round(value, 5), "unit": "TFLOP/s", "cores": orc.max_threads(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 

@@ -232,6 +232,104 @@ int vsa_aggregate_probs_to_cubes(const vsa_layout_t* layout, int64_t bh, const f
 int vsa_selection_accuracy(const vsa_layout_t* layout, int64_t bh, const float* probs_cube, const int32_t* sel,
                            int64_t top_k, double* acc, void* stream);
 
+/* ============================================================================
+ * The operator context (SURVEY.md §8b "device-side context"): vsa_forward /
+ * vsa_backward (vsa.hpp:89-93, 129-133) with the forward artifacts (the VsaOutput of
+ * vsa.hpp:56-63: pooled cubes, Ac, Oc, block map + transposed map, fine output, lse,
+ * gates) resident in HBM between the two calls. One context per (layout, shape); the
+ * calls are stream-ordered and asynchronous.
+ * ========================================================================== */
+typedef struct vsa_op vsa_op_t;
+
+enum {
+  VSA_OP_FORCE_SIMT = 1,       /* SIMT fine kernels (fp32 parity mode / debug) even for bf16 */
+  VSA_OP_NO_DS_WORKSPACE = 2   /* backward recomputes S / dP for dQ even when a workspace is attached */
+};
+
+typedef struct vsa_op_desc_t {
+  int64_t batch, heads, head_dim;
+  int64_t top_k;       /* VsaParams::top_k (vsa.hpp:20), 1 <= top_k <= nc */
+  int64_t max_sel_k;   /* largest k of a sel_override (0 = top_k) */
+  int64_t model_dim;   /* > 0: the gate projection of vsa_forward / vsa_backward (VsaParams::gate_weight rows) */
+  int32_t dtype;       /* VSA_BF16 (tcgen05) or VSA_F32 (parity mode) */
+  int32_t pool_mode;   /* VsaParams::pool (vsa.hpp:21) */
+  int32_t activation;  /* VsaParams::activation (vsa.hpp:22) */
+  int32_t adaptation;  /* VsaParams::adaptation (vsa.hpp:23): Gf == 1 */
+  int32_t raster;      /* 1: q/k/v/gates/out/dO/grads raster-ordered (tiling fused); 0: tile-ordered (vsa.hpp:86) */
+  int32_t flags;       /* VSA_OP_* */
+} vsa_op_desc_t;
+
+/* Device pointers of the context's buffers (views for callers and tests). */
+typedef struct vsa_op_buffers_t {
+  void* base;
+  size_t bytes;
+  void *q_t, *k_t, *v_t;                /* tiled copies (raster mode), else NULL */
+  float *qc, *kc, *vc, *ac, *oc_cube;   /* CoarseArtifacts (coarse.hpp:18-25), Oc at cube level */
+  int32_t *sel, *selT_offs, *selT_idx;  /* coarse top-k map, transposed CSR map of the map the fine stage used */
+  void* o_fine;                         /* FineResult::out, tiled */
+  float* lse;                           /* FineSaved::row_lse [B*H, Lp] */
+  void* dof;
+  float *delta, *doc_cube, *dqc, *dkc, *dvc;
+  void *gc, *gf, *dgc, *dgf;            /* gates (model_dim > 0) */
+  const int32_t* fine_sel;              /* selection the fine stage used (VsaOutput::fine_sel) */
+  int64_t fine_k;
+  int32_t bwd_used_workspace;           /* last backward: 1 = dS workspace path, 0 = recompute */
+} vsa_op_buffers_t;
+
+/* Bytes of device memory vsa_op_create needs (0 for an invalid descriptor). */
+size_t vsa_op_memory_bytes(const vsa_layout_t* layout, const vsa_op_desc_t* desc);
+/* device_memory: caller-owned block of >= vsa_op_memory_bytes, or NULL (the op cudaMallocs
+ * and frees it). The layout (with its raster I/O order) is copied. */
+int vsa_op_create(const vsa_layout_t* layout, const vsa_op_desc_t* desc, void* device_memory, size_t bytes,
+                  vsa_op_t** op);
+int vsa_op_destroy(vsa_op_t* op);
+int vsa_op_buffers(const vsa_op_t* op, vsa_op_buffers_t* out);
+/* dS workspace of the backward (>= vsa_op_workspace_bytes(op, k)); NULL = recompute path. */
+int vsa_op_set_workspace(vsa_op_t* op, void* ws, size_t bytes);
+size_t vsa_op_workspace_bytes(const vsa_op_t* op, int64_t sel_k);
+
+/* Attention-level forward (gates given): K1-K3 (vsa_op_forward_coarse) then K4+K5
+ * (vsa_op_forward_fine). sel_override (vsa.hpp:93,115): device int32 [B*H, nc, sel_k]
+ * replacing the fine stage's map (the coarse stage still computes its own top-k); it is
+ * validated with one synchronous flag read. */
+int vsa_op_forward(vsa_op_t* op, const void* q, const void* k, const void* v, const void* gc, const void* gf,
+                   const int32_t* sel_override, int64_t sel_k, void* out, void* stream);
+int vsa_op_forward_coarse(vsa_op_t* op, const void* q, const void* k, const void* v, const int32_t* sel_override,
+                          int64_t sel_k, void* stream);
+int vsa_op_forward_fine(vsa_op_t* op, const void* gc, const void* gf, void* out, void* stream);
+/* Attention-level backward: dO -> dq, dk, dv, dgc, dgf (dgc/dgf may be NULL). */
+int vsa_op_backward(vsa_op_t* op, const void* dout, void* dq, void* dk, void* dv, void* dgc, void* dgf,
+                    void* stream);
+
+/* Replaces: vsa_forward (vsa.hpp:89-122). hidden: bf16 [B, S, model_dim] in the op's row
+ * order (raster tokens, or tile order when desc.raster == 0); gate_weight bf16
+ * [model_dim, 2*H*d]; gate_bias fp32 [2*H*d] or NULL. The gates stay in the context. */
+int vsa_forward(vsa_op_t* op, const void* hidden, const void* gate_weight, const float* gate_bias, const void* q,
+                const void* k, const void* v, const int32_t* sel_override, int64_t sel_k, void* out, void* stream);
+/* Replaces: vsa_backward (vsa.hpp:129-189): dq, dk, dv (coarse + fine paths), dhidden
+ * bf16 [B, S, model_dim], dgate_weight fp32 [model_dim, 2*H*d], dgate_bias fp32 or NULL.
+ * Missing forward artifacts -> VSA_EINVAL (vsa.hpp:137-138). */
+int vsa_backward(vsa_op_t* op, const void* hidden, const void* gate_weight, const void* dout, void* dq, void* dk,
+                 void* dv, void* dhidden, float* dgate_weight, float* dgate_bias, void* stream);
+
+/* Stage timing without host gaps: with timing on, each call records CUDA events between
+ * its stages on the launch stream; vsa_op_stage_ms synchronises once and returns the mean
+ * per stage over the timed calls: [tile_pool, coarse_fwd, fine_fwd, prologue, coarse_bwd,
+ * fine_bwd]. calls (nullable) = {forward calls, backward calls}. */
+enum { VSA_OP_STAGES = 6 };
+int vsa_op_timing(vsa_op_t* op, int32_t enable);
+int vsa_op_stage_ms(vsa_op_t* op, float* ms, int32_t* calls);
+
+/* Replaces the token-level coarse_backward (coarse.hpp:124-184) on tile-ordered tensors:
+ * doc tiled [B*H, Lp, d] -> cube sums -> K6d -> unpool (mean: broadcast dxc/cube; max:
+ * first argmax token of x_tiled) into dq, dk, dv tiled. Scratch fp32: doc_cube, dqc,
+ * dkc, dvc [B*H, nc, d] and [B*H, nc, nc]. q/k/v tiled are needed for max pooling only. */
+int vsa_coarse_backward_tokens(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const float* qc,
+                               const float* kc, const float* vc, const float* ac, int32_t pool_mode,
+                               const void* doc, const void* q_t, const void* k_t, const void* v_t, float* doc_cube,
+                               float* dqc, float* dkc, float* dvc, float* scratch, void* dq, void* dk, void* dv,
+                               void* stream);
+
 /* Ulysses resharding copy: dst[i1][i0] = src[i0][i1] over an
  * [n0][n1] grid of contiguous blocks of `block_bytes` (a multiple of 16). With
  * n0 = B*S/P, n1 = P, block = (H/P)*d*elem it packs a sequence shard [B,S/P,H,d]

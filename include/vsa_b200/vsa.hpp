@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -67,6 +68,16 @@ class DeviceBuffer {
   DeviceBuffer(const DeviceBuffer&) = delete;
   DeviceBuffer& operator=(const DeviceBuffer&) = delete;
   DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+      if (p_) cudaFree(p_);
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
   ~DeviceBuffer() {
     if (p_) cudaFree(p_);
   }
@@ -363,6 +374,274 @@ CoarseArtifacts coarse_forward_select(const TileLayout& layout, const AttnTensor
   ac.to_host(art.ac.data()); oc.to_host(art.oc_cube.data());
   sel.to_host(art.sel.data());
   return art;
+}
+
+// fine_backward with the reference signature (fine.hpp:107-111): only the saved
+// softmax statistics are given, so the fine output (needed for delta = rowsum(dO * O))
+// is recomputed by one fine forward on the device.
+template <typename Scalar>
+AttnGrads<Scalar> fine_backward(const TileLayout& layout, const AttnTensor<Scalar>& q, const AttnTensor<Scalar>& k,
+                                const AttnTensor<Scalar>& v, const BlockSelection& sel,
+                                const AttnTensor<Scalar>& dout, const SoftmaxStats& saved) {
+  FineResult<Scalar> fwd = fine_forward(layout, q, k, v, sel);
+  detail::require(saved.row_lse.size() == fwd.saved.row_lse.size(),
+                  "fine_backward: saved statistics do not match shapes");
+  fwd.saved.row_lse = saved.row_lse;  // the caller's lse drives the backward, as in the reference
+  return fine_backward(layout, q, k, v, sel, dout, fwd);
+}
+
+// pool_cubes (coarse.hpp:47-65) on a tile-ordered tensor -> fp32 [B, H, nc, d].
+template <typename Scalar>
+AttnTensor<float> pool_cubes(const TileLayout& layout, const AttnTensor<Scalar>& x, PoolMode mode = PoolMode::kMean) {
+  detail::require(x.seq() == layout.seq_len, "pool_cubes: sequence length does not match layout");
+  const Index bh = x.batch() * x.heads();
+  detail::DeviceBuffer<Scalar> dx(x.data(), x.size());
+  AttnTensor<float> out(x.batch(), x.heads(), layout.num_cubes, x.dim());
+  detail::DeviceBuffer<float> dp(out.size());
+  detail::check(vsa_pool_tiled(layout.raw(), bh, x.dim(), detail::dtype_of<Scalar>(), dx.get(), dp.get(),
+                               mode == PoolMode::kMean ? VSA_POOL_MEAN : VSA_POOL_MAX, nullptr));
+  dp.to_host(out.data());
+  return out;
+}
+
+// coarse_backward (coarse.hpp:124-184): token-level dOc (tile-ordered) -> (dq, dk, dv).
+template <typename Scalar>
+AttnGrads<Scalar> coarse_backward(const CoarseArtifacts& art, const TileLayout& layout,
+                                  const AttnTensor<Scalar>& doc, const AttnTensor<Scalar>& q,
+                                  const AttnTensor<Scalar>& k, const AttnTensor<Scalar>& v) {
+  detail::require(doc.same_shape(q), "coarse_backward: dOc shape mismatch");
+  const Index bh = q.batch() * q.heads(), d = q.dim(), nc = layout.num_cubes, n = q.size();
+  detail::require(static_cast<Index>(art.ac.size()) == bh * nc * nc, "coarse_backward: artifacts do not match layout");
+  const int32_t dt = detail::dtype_of<Scalar>();
+  detail::DeviceBuffer<float> qc(art.qc.data(), art.qc.size()), kc(art.kc.data(), art.kc.size()),
+      vc(art.vc.data(), art.vc.size()), ac(art.ac.data(), art.ac.size()), docc(bh * nc * d), dqc(bh * nc * d),
+      dkc(bh * nc * d), dvc(bh * nc * d), scratch(bh * nc * nc);
+  detail::DeviceBuffer<Scalar> ddoc(doc.data(), n), dq_(q.data(), n), dk_(k.data(), n), dv_(v.data(), n), gq(n),
+      gk(n), gv(n);
+  detail::check(vsa_coarse_backward_tokens(layout.raw(), bh, d, dt, qc.get(), kc.get(), vc.get(), ac.get(),
+                                           art.pool == PoolMode::kMean ? VSA_POOL_MEAN : VSA_POOL_MAX, ddoc.get(),
+                                           dq_.get(), dk_.get(), dv_.get(), docc.get(), dqc.get(), dkc.get(),
+                                           dvc.get(), scratch.get(), gq.get(), gk.get(), gv.get(), nullptr));
+  AttnGrads<Scalar> g{AttnTensor<Scalar>(q.batch(), q.heads(), q.seq(), d),
+                      AttnTensor<Scalar>(q.batch(), q.heads(), q.seq(), d),
+                      AttnTensor<Scalar>(q.batch(), q.heads(), q.seq(), d)};
+  gq.to_host(g.dq.data());
+  gk.to_host(g.dk.data());
+  gv.to_host(g.dv.data());
+  return g;
+}
+
+// ============================================================================ the operator
+enum class GateActivation { kIdentity, kSigmoid };  // vsa.hpp:9
+
+// VsaParams (vsa.hpp:16-52). gate_weight is row-major [model_dim, 2*heads*head_dim] on the
+// host; the gate projection runs on the tcgen05 GEMM in bf16.
+template <typename Scalar>
+struct VsaParams {
+  Index model_dim = 0, cols = 0;
+  std::vector<float> gate_weight;  // [model_dim][cols]
+  std::vector<float> gate_bias;    // empty or [cols]
+  Index top_k = 1;
+  PoolMode pool = PoolMode::kMean;
+  GateActivation activation = GateActivation::kIdentity;
+  bool adaptation = false;
+
+  // random_init (vsa.hpp:25-32): the reference's draws (randn_matrix, tensor.hpp:126-133).
+  static VsaParams random_init(Index model_dim, Index heads, Index head_dim, Index top_k, std::mt19937_64& rng) {
+    VsaParams p;
+    p.model_dim = model_dim;
+    p.cols = 2 * heads * head_dim;
+    p.gate_weight.resize(static_cast<size_t>(model_dim * p.cols));
+    std::normal_distribution<double> dist(0.0, 1.0 / std::sqrt(static_cast<double>(model_dim)));
+    for (auto& w : p.gate_weight) w = static_cast<float>(static_cast<Scalar>(static_cast<float>(dist(rng))));
+    p.top_k = top_k;
+    return p;
+  }
+  // adaptation_init (vsa.hpp:35-42): zero weights, fine gate fixed to one, k = all cubes.
+  static VsaParams adaptation_init(Index model_dim, Index heads, Index head_dim, Index num_cubes) {
+    VsaParams p;
+    p.model_dim = model_dim;
+    p.cols = 2 * heads * head_dim;
+    p.gate_weight.assign(static_cast<size_t>(model_dim * p.cols), 0.f);
+    p.top_k = num_cubes;
+    p.adaptation = true;
+    return p;
+  }
+  void check(Index md, Index heads, Index head_dim) const {
+    detail::require(model_dim == md && cols == 2 * heads * head_dim &&
+                        static_cast<Index>(gate_weight.size()) == md * cols,
+                    "VsaParams: gate projection must map model_dim -> 2*heads*head_dim");
+    detail::require(gate_bias.empty() || static_cast<Index>(gate_bias.size()) == cols,
+                    "VsaParams: gate bias size mismatch");
+    detail::require(top_k >= 1, "VsaParams: k must be >= 1");
+  }
+};
+
+namespace detail {
+// The device operator context (vsa_op_t) with RAII.
+struct OpHandle {
+  vsa_op_t* op = nullptr;
+  DeviceBuffer<uint8_t> ws;
+  // the forward's device inputs (the context's artifacts point into q/k/v; the backward
+  // reuses them, as the reference's vsa_backward receives the same q, k, v, hidden)
+  DeviceBuffer<bf16> hidden, q, k, v, w;
+  DeviceBuffer<float> bias;
+  ~OpHandle() {
+    if (op) vsa_op_destroy(op);
+  }
+};
+}  // namespace detail
+
+// VsaOutput (vsa.hpp:56-63): host copies of the output and artifacts; the device
+// context `ctx` keeps them resident for vsa_backward.
+template <typename Scalar>
+struct VsaOutput {
+  AttnTensor<Scalar> out;
+  CoarseArtifacts coarse;
+  FineResult<Scalar> fine;
+  AttnTensor<Scalar> gate_coarse, gate_fine;
+  BlockSelection fine_sel;
+  std::shared_ptr<detail::OpHandle> ctx;
+};
+
+// VsaGrads (vsa.hpp:65-71).
+template <typename Scalar>
+struct VsaGrads {
+  AttnTensor<Scalar> dq, dk, dv;
+  AttnTensor<Scalar> dhidden;          // [batch, 1, seq, model_dim]
+  std::vector<float> dgate_weight;     // [model_dim][2*heads*head_dim]
+  std::vector<float> dgate_bias;       // empty or [2*heads*head_dim]
+};
+
+namespace detail {
+template <typename Scalar>
+void check_hidden(const AttnTensor<Scalar>& hidden, const AttnTensor<Scalar>& q) {  // vsa.hpp:75-80
+  require(hidden.heads() == 1, "vsa: hidden states are [batch, 1, seq, model_dim]");
+  require(hidden.batch() == q.batch() && hidden.seq() == q.seq(), "vsa: hidden states do not match Q/K/V shapes");
+}
+inline std::vector<bf16> to_bf16(const std::vector<float>& x) {
+  std::vector<bf16> y(x.size());
+  for (size_t i = 0; i < x.size(); ++i) y[i] = __float2bfloat16(x[i]);
+  return y;
+}
+}  // namespace detail
+
+// vsa_forward (vsa.hpp:89-122): q, k, v, hidden tile-ordered. Scalar = bf16 (the gate
+// projection is a bf16 tcgen05 GEMM; the attention stages run the tcgen05 path).
+template <typename Scalar>
+VsaOutput<Scalar> vsa_forward(const TileLayout& layout, const AttnTensor<Scalar>& hidden, const AttnTensor<Scalar>& q,
+                              const AttnTensor<Scalar>& k, const AttnTensor<Scalar>& v,
+                              const VsaParams<Scalar>& params, const BlockSelection* sel_override = nullptr) {
+  static_assert(std::is_same_v<Scalar, bf16>, "vsa_b200::vsa_forward: the gate projection runs in bf16");
+  detail::require(q.size() > 0, "attention: empty tensors");
+  detail::require(q.same_shape(k) && q.same_shape(v), "attention: Q, K, V must share one shape");
+  detail::check_hidden(hidden, q);
+  const Index B = q.batch(), H = q.heads(), S = q.seq(), d = q.dim(), nc = layout.num_cubes, md = hidden.dim();
+  detail::require(S == layout.seq_len, "vsa: sequence length does not match layout");
+  params.check(md, H, d);
+  detail::require(params.top_k <= nc, "coarse_forward_select: k must be in [1, num_cubes]");
+  if (sel_override) {
+    detail::require(sel_override->batch() == B && sel_override->heads() == H && sel_override->num_cubes() == nc,
+                    "fine stage: selection does not match shapes");
+    sel_override->validate();
+  }
+  vsa_op_desc_t desc{};
+  desc.batch = B;
+  desc.heads = H;
+  desc.head_dim = d;
+  desc.top_k = params.top_k;
+  desc.max_sel_k = sel_override ? sel_override->k() : 0;
+  desc.model_dim = md;
+  desc.dtype = VSA_BF16;
+  desc.pool_mode = params.pool == PoolMode::kMean ? VSA_POOL_MEAN : VSA_POOL_MAX;
+  desc.activation = params.activation == GateActivation::kSigmoid ? VSA_GATE_SIGMOID : VSA_GATE_IDENTITY;
+  desc.adaptation = params.adaptation ? 1 : 0;
+  desc.raster = 0;  // the reference contract: tile-ordered tensors (vsa.hpp:86)
+  VsaOutput<Scalar> res;
+  res.ctx = std::make_shared<detail::OpHandle>();
+  detail::check(vsa_op_create(layout.raw(), &desc, nullptr, 0, &res.ctx->op));
+  const size_t n = static_cast<size_t>(q.size());
+  auto& c = *res.ctx;
+  c.hidden = detail::DeviceBuffer<bf16>(hidden.data(), static_cast<size_t>(hidden.size()));
+  c.q = detail::DeviceBuffer<bf16>(q.data(), n);
+  c.k = detail::DeviceBuffer<bf16>(k.data(), n);
+  c.v = detail::DeviceBuffer<bf16>(v.data(), n);
+  const auto wb = detail::to_bf16(params.gate_weight);
+  c.w = detail::DeviceBuffer<bf16>(wb.data(), wb.size());
+  c.bias = detail::DeviceBuffer<float>(params.gate_bias.data(), params.gate_bias.size());
+  detail::DeviceBuffer<Scalar> dout(n);
+  detail::DeviceBuffer<int32_t> dsel(sel_override ? sel_override->data() : nullptr,
+                                     sel_override ? static_cast<size_t>(B * H * nc * sel_override->k()) : 0);
+  detail::check(::vsa_forward(c.op, c.hidden.get(), c.w.get(), params.gate_bias.empty() ? nullptr : c.bias.get(),
+                            c.q.get(), c.k.get(), c.v.get(), sel_override ? dsel.get() : nullptr,
+                            sel_override ? sel_override->k() : 0, dout.get(), nullptr));
+  detail::cuda(cudaDeviceSynchronize());
+  vsa_op_buffers_t b{};
+  detail::check(vsa_op_buffers(res.ctx->op, &b));
+  auto d2h = [](void* dst, const void* src, size_t bytes) {
+    detail::cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  };
+  res.out = AttnTensor<Scalar>(B, H, S, d);
+  dout.to_host(res.out.data());
+  const size_t cub = static_cast<size_t>(B * H * nc * d), es = sizeof(Scalar);
+  res.coarse.pool = params.pool;
+  res.coarse.qc.resize(cub); res.coarse.kc.resize(cub); res.coarse.vc.resize(cub); res.coarse.oc_cube.resize(cub);
+  res.coarse.ac.resize(static_cast<size_t>(B * H * nc * nc));
+  d2h(res.coarse.qc.data(), b.qc, cub * 4); d2h(res.coarse.kc.data(), b.kc, cub * 4);
+  d2h(res.coarse.vc.data(), b.vc, cub * 4); d2h(res.coarse.oc_cube.data(), b.oc_cube, cub * 4);
+  d2h(res.coarse.ac.data(), b.ac, res.coarse.ac.size() * 4);
+  res.coarse.sel = BlockSelection(B, H, nc, params.top_k);
+  d2h(res.coarse.sel.data(), b.sel, static_cast<size_t>(B * H * nc * params.top_k) * 4);
+  res.fine.out = AttnTensor<Scalar>(B, H, S, d);
+  d2h(res.fine.out.data(), b.o_fine, n * es);
+  res.fine.saved.row_lse.resize(static_cast<size_t>(B * H * S));
+  d2h(res.fine.saved.row_lse.data(), b.lse, res.fine.saved.row_lse.size() * 4);
+  res.gate_coarse = AttnTensor<Scalar>(B, H, S, d);
+  res.gate_fine = AttnTensor<Scalar>(B, H, S, d);
+  d2h(res.gate_coarse.data(), b.gc, n * es);
+  d2h(res.gate_fine.data(), b.gf, n * es);
+  res.fine_sel = sel_override ? *sel_override : res.coarse.sel;
+  return res;
+}
+
+// vsa_backward (vsa.hpp:129-189) on the device artifacts of `fwd`.
+template <typename Scalar>
+VsaGrads<Scalar> vsa_backward(const TileLayout& layout, const VsaOutput<Scalar>& fwd, const AttnTensor<Scalar>& hidden,
+                              const AttnTensor<Scalar>& q, const AttnTensor<Scalar>& k, const AttnTensor<Scalar>& v,
+                              const VsaParams<Scalar>& params, const AttnTensor<Scalar>& dout) {
+  detail::require(q.same_shape(k) && q.same_shape(v), "attention: Q, K, V must share one shape");
+  detail::check_hidden(hidden, q);
+  detail::require(dout.same_shape(q), "vsa_backward: dO shape mismatch");
+  detail::require(fwd.ctx && fwd.ctx->op && fwd.out.same_shape(q) && !fwd.fine_sel.empty(),
+                  "vsa_backward: missing or mismatched forward artifacts");
+  const Index B = q.batch(), H = q.heads(), S = q.seq(), d = q.dim(), md = hidden.dim();
+  params.check(md, H, d);
+  (void)layout;
+  vsa_op_t* op = fwd.ctx->op;
+  const size_t wsb = vsa_op_workspace_bytes(op, fwd.fine_sel.k());
+  if (fwd.ctx->ws.size() < wsb) {
+    fwd.ctx->ws = detail::DeviceBuffer<uint8_t>(wsb);
+    detail::check(vsa_op_set_workspace(op, fwd.ctx->ws.get(), wsb));
+  }
+  const size_t n = static_cast<size_t>(q.size());
+  auto& c = *fwd.ctx;
+  detail::DeviceBuffer<Scalar> ddo(dout.data(), n), gq(n), gk(n), gv(n), gh(static_cast<size_t>(hidden.size()));
+  detail::DeviceBuffer<float> gW(params.gate_weight.size()), gb(params.gate_bias.size());
+  detail::check(::vsa_backward(op, c.hidden.get(), c.w.get(), ddo.get(), gq.get(), gk.get(), gv.get(), gh.get(),
+                             gW.get(), params.gate_bias.empty() ? nullptr : gb.get(), nullptr));
+  detail::cuda(cudaDeviceSynchronize());
+  VsaGrads<Scalar> g{AttnTensor<Scalar>(B, H, S, d), AttnTensor<Scalar>(B, H, S, d), AttnTensor<Scalar>(B, H, S, d),
+                     AttnTensor<Scalar>(B, 1, S, md), std::vector<float>(params.gate_weight.size()), {}};
+  gq.to_host(g.dq.data());
+  gk.to_host(g.dk.data());
+  gv.to_host(g.dv.data());
+  gh.to_host(g.dhidden.data());
+  gW.to_host(g.dgate_weight.data());
+  if (!params.gate_bias.empty()) {
+    g.dgate_bias.resize(params.gate_bias.size());
+    gb.to_host(g.dgate_bias.data());
+  }
+  return g;
 }
 
 }  // namespace vsa_b200

@@ -29,6 +29,22 @@ class vsa_layout_t(C.Structure):
         ("io_chunk", C.c_int64)]
 
 
+class vsa_op_desc_t(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("batch", "heads", "head_dim", "top_k", "max_sel_k", "model_dim")] + [
+        (n, C.c_int32) for n in ("dtype", "pool_mode", "activation", "adaptation", "raster", "flags")]
+
+
+class vsa_op_buffers_t(C.Structure):
+    _fields_ = [("base", C.c_void_p), ("bytes", C.c_size_t)] + [
+        (n, C.c_void_p) for n in ("q_t", "k_t", "v_t", "qc", "kc", "vc", "ac", "oc_cube", "sel", "selT_offs",
+                                  "selT_idx", "o_fine", "lse", "dof", "delta", "doc_cube", "dqc", "dkc", "dvc",
+                                  "gc", "gf", "dgc", "dgf", "fine_sel")] + [
+        ("fine_k", C.c_int64), ("bwd_used_workspace", C.c_int32)]
+
+
+OP_FORCE_SIMT, OP_NO_DS_WORKSPACE = 1, 2
+OP_STAGES = ["tile_pool", "coarse_fwd", "fine_fwd", "prologue", "coarse_bwd", "fine_bwd"]
+
 EXPORTS = [
     "vsa_last_error", "vsa_version", "vsa_kernel_launches", "vsa_debug_trace", "vsa_layout_make", "vsa_flatten_index", "vsa_tile", "vsa_untile",
     "vsa_tile_pool", "vsa_pool_tiled", "vsa_coarse_forward", "vsa_coarse_bitmap_bytes", "vsa_selection_transpose",
@@ -36,6 +52,9 @@ EXPORTS = [
     "vsa_fine_backward", "vsa_fine_backward_workspace_bytes", "vsa_unpool_max_add", "vsa_layout_set_io",
     "vsa_transpose_blocks", "vsa_gate_forward", "vsa_gate_backward", "vsa_gate_backward_workspace_bytes",
     "vsa_selection_accuracy_from_lse", "vsa_aggregate_probs_to_cubes", "vsa_selection_accuracy",
+    "vsa_op_memory_bytes", "vsa_op_create", "vsa_op_destroy", "vsa_op_buffers", "vsa_op_set_workspace",
+    "vsa_op_workspace_bytes", "vsa_op_forward", "vsa_op_forward_coarse", "vsa_op_forward_fine", "vsa_op_backward",
+    "vsa_forward", "vsa_backward", "vsa_op_timing", "vsa_op_stage_ms", "vsa_coarse_backward_tokens",
 ]
 
 
@@ -92,6 +111,19 @@ def lib():
         "vsa_fine_backward": [LP, I64, I64, I32, P, P, P, P, P, P, P, I64, P, P, P, P, P, I32, I32, P, P, P, P,
                               C.c_size_t, P],
         "vsa_unpool_max_add": [LP, I64, I64, I32, P, P, I32, P, P],
+        "vsa_op_create": [LP, C.POINTER(vsa_op_desc_t), P, C.c_size_t, C.POINTER(P)],
+        "vsa_op_destroy": [P],
+        "vsa_op_buffers": [P, C.POINTER(vsa_op_buffers_t)],
+        "vsa_op_set_workspace": [P, P, C.c_size_t],
+        "vsa_op_forward": [P, P, P, P, P, P, P, I64, P, P],
+        "vsa_op_forward_coarse": [P, P, P, P, P, I64, P],
+        "vsa_op_forward_fine": [P, P, P, P, P],
+        "vsa_op_backward": [P, P, P, P, P, P, P, P],
+        "vsa_forward": [P, P, P, P, P, P, P, P, I64, P, P],
+        "vsa_backward": [P, P, P, P, P, P, P, P, P, P, P],
+        "vsa_op_timing": [P, I32],
+        "vsa_op_stage_ms": [P, C.POINTER(C.c_float), C.POINTER(I32)],
+        "vsa_coarse_backward_tokens": [LP, I64, I64, I32, P, P, P, P, I32, P, P, P, P, P, P, P, P, P, P, P, P, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -102,6 +134,10 @@ def lib():
     L.vsa_fine_backward_workspace_bytes.argtypes = [LP, I64, I64]
     L.vsa_fine_backward_workspace_bytes.restype = C.c_size_t
     L.vsa_gate_backward_workspace_bytes.restype = C.c_size_t
+    L.vsa_op_memory_bytes.argtypes = [LP, C.POINTER(vsa_op_desc_t)]
+    L.vsa_op_memory_bytes.restype = C.c_size_t
+    L.vsa_op_workspace_bytes.argtypes = [P, I64]
+    L.vsa_op_workspace_bytes.restype = C.c_size_t
     _lib = L
     return L
 

@@ -229,7 +229,9 @@ def coarse_forward_select(layout: TileLayout, q, k, v, top_k: int, mode: int = P
 
 
 def coarse_backward(art: CoarseArtifacts, layout: TileLayout, doc, q, k, v):
-    """coarse_backward (coarse.hpp:124-184): token-level dOc (tiled) -> tiled (dq, dk, dv)."""
+    """coarse_backward (coarse.hpp:124-184): token-level dOc (tiled) -> tiled (dq, dk, dv).
+    Cube sums, the cube-level backward and the unpool all run in the library
+    (vsa_coarse_backward_tokens)."""
     _cuda4(doc, "coarse_backward")
     if doc.shape != q.shape:
         raise ValueError("coarse_backward: dOc shape mismatch")
@@ -237,20 +239,15 @@ def coarse_backward(art: CoarseArtifacts, layout: TileLayout, doc, q, k, v):
         raise ValueError("coarse_backward: artifacts do not match layout")
     B, H, _, d = q.shape
     nc = layout.num_cubes
-    doc_cube = pool_cubes(layout, doc, POOL_MEAN) * float(layout.cube_size)  # sum over tokens
-    dqc, dkc, dvc = (torch.empty((B, H, nc, d), dtype=torch.float32, device=q.device) for _ in range(3))
-    scratch = torch.empty((B, H, nc, nc), dtype=torch.float32, device=q.device)
-    check(L.lib().vsa_coarse_backward(layout.ref(), B * H, d, _p(art.qc), _p(art.kc), _p(art.vc), _p(art.ac),
-                                      _p(doc_cube), _p(dqc), _p(dkc), _p(dvc), _p(scratch), _stream()))
-    outs = []
-    for dc, x in ((dqc, q), (dkc, k), (dvc, v)):
-        if art.pool == POOL_MEAN:
-            outs.append((dc / float(layout.cube_size)).repeat_interleave(layout.cube_size, dim=2).to(q.dtype))
-        else:
-            dx = torch.zeros_like(x)
-            check(L.lib().vsa_unpool_max_add(layout.ref(), B * H, d, _dt(x), _p(x), _p(dc), 0, _p(dx), _stream()))
-            outs.append(dx)
-    return tuple(outs)
+    f32 = lambda *s: torch.empty(s, dtype=torch.float32, device=q.device)
+    doc_cube, dqc, dkc, dvc = (f32(B, H, nc, d) for _ in range(4))
+    scratch = f32(B, H, nc, nc)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    check(L.lib().vsa_coarse_backward_tokens(layout.ref(), B * H, d, _dt(q), _p(art.qc), _p(art.kc), _p(art.vc),
+                                             _p(art.ac), int(art.pool), _p(doc), _p(q), _p(k), _p(v), _p(doc_cube),
+                                             _p(dqc), _p(dkc), _p(dvc), _p(scratch), _p(dq), _p(dk), _p(dv),
+                                             _stream()))
+    return dq, dk, dv
 
 
 # ----------------------------------------------------------------------------- fine
@@ -327,74 +324,141 @@ def fine_backward(layout: TileLayout, q, k, v, sel, dout, row_lse, out=None, sel
 class VsaOp:
     """The VSA attention operator on device-resident buffers: the hot path.
 
+    A thin wrapper over the native operator context (``vsa_op_*`` in
+    include/vsa_b200.h, csrc/op.cu), which orchestrates the stage kernels and keeps
+    the forward artifacts (the VsaOutput of vsa.hpp:56-63) resident in HBM. Its
+    device memory is one block from torch's caching allocator; the attributes
+    (``sel``, ``lse``, ``ac``, ...) are views into it.
+
     forward(q, k, v, gc, gf) -> O and backward(dO) -> (dQ, dK, dV, dGc, dGf), all
     raster-ordered [B, H, t*h*w, d] (``raster=True``, tiling fused into K1 and the
     fine epilogue) or tile-ordered (``raster=False``, the reference's vsa_forward
-    contract, vsa.hpp:86). Buffers are allocated once (HBM-resident artifacts,
-    the VsaOutput of vsa.hpp:56-63).
+    contract, vsa.hpp:86).
 
     ``io="bshd"`` (raster only) reads and writes the raster tensors sequence-major
     instead: [B, S, H, d] (DiT-native), or with ``seq_chunks=P`` the
     Ulysses receive layout [P, B, S/P, H, d] (§8e) — consumed in place, no copies.
+    ``model_dim > 0`` adds the gate projection (``forward_hidden`` / ``backward_hidden``,
+    the reference's vsa_forward / vsa_backward with hidden states and VsaParams).
     """
 
     def __init__(self, layout: TileLayout, B: int, H: int, d: int, top_k: int, dtype=torch.bfloat16,
                  pool: int = POOL_MEAN, adaptation: bool = False, raster: bool = True, device="cuda",
-                 force_simt: bool = False, bwd_workspace: bool = True, io: str = "bhsd", seq_chunks: int = 1):
+                 force_simt: bool = False, bwd_workspace: bool = True, io: str = "bhsd", seq_chunks: int = 1,
+                 max_sel_k: int = 0, model_dim: int = 0, activation: int = GATE_IDENTITY):
         if not (1 <= top_k <= layout.num_cubes):
             raise ValueError("coarse_forward_select: k must be in [1, num_cubes]")
         if io not in ("bhsd", "bshd"):
             raise ValueError("io must be 'bhsd' or 'bshd'")
         if io == "bshd" and not raster:
             raise ValueError("sequence-major I/O needs raster=True")
+        if dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError(f"unsupported dtype {dtype} (bf16 or fp32)")
         self.io, self.seq_chunks = io, int(seq_chunks)
         self.layout, self.B, self.H, self.d, self.top_k = layout, B, H, d, int(top_k)
         self.dtype, self.pool, self.adaptation, self.raster = dtype, pool, adaptation, raster
         self.force_simt = force_simt
+        self.model_dim, self.activation = int(model_dim), int(activation)
         # dS-materialising backward workspace (B*H*nc*k bf16 64x64 tiles), allocated on first backward
         self.bwd_workspace = bwd_workspace
         self.ws = None
-        nc, Lp = layout.num_cubes, layout.seq_padded
-        e = lambda *s, dt=dtype: torch.empty(s, dtype=dt, device=device)
-        f32, i32 = torch.float32, torch.int32
-        self.q_t, self.k_t, self.v_t = e(B, H, Lp, d), e(B, H, Lp, d), e(B, H, Lp, d)
-        self.qc, self.kc, self.vc = e(B, H, nc, d, dt=f32), e(B, H, nc, d, dt=f32), e(B, H, nc, d, dt=f32)
-        self.ac = e(B, H, nc, nc, dt=f32)
-        self.oc = e(B, H, nc, d, dt=f32)
-        self.sel = e(B, H, nc, self.top_k, dt=i32)
-        self.selT_offs = e(B * H, nc + 1, dt=i32)
-        self.selT_idx = e(B * H, nc * self.top_k, dt=i32)
-        self.bitmap = e(max(1, L.lib().vsa_coarse_bitmap_bytes(layout.ref(), B * H)), dt=torch.uint8)
-        self.o_f = e(B, H, Lp, d)
-        self.lse = e(B, H, Lp, dt=f32)
-        self.dof = e(B, H, Lp, d)
-        self.delta = e(B, H, Lp, dt=f32)
-        self.doc = e(B, H, nc, d, dt=f32)
-        self.dqc, self.dkc, self.dvc = e(B, H, nc, d, dt=f32), e(B, H, nc, d, dt=f32), e(B, H, nc, d, dt=f32)
-        self.scratch = e(B, H, nc, nc, dt=f32)
-        self.fine_sel = self.sel
-        self.fine_k = self.top_k
-        self._gc = self._gf = None
+        self.device = torch.device(device)
         self._lib = L.lib()
-        self._lref = layout.ref()
         S = layout.seq_len
+        self._raw = L.vsa_layout_t.from_buffer_copy(layout._raw)
         if io == "bshd":
             if self.seq_chunks < 1 or S % self.seq_chunks:
                 raise ValueError("seq_chunks must divide the raster sequence length")
-            self._raw = L.vsa_layout_t.from_buffer_copy(layout._raw)
             check(self._lib.vsa_layout_set_io(C.byref(self._raw), L.IO_SEQ_MAJOR, B, H, S // self.seq_chunks))
-            self._lref = C.byref(self._raw)
             self.io_shape = ((B, S, H, d) if self.seq_chunks == 1 else
                              (self.seq_chunks, B, S // self.seq_chunks, H, d))
         else:
             self.io_shape = (B, H, S if raster else layout.seq_padded, d)
-        self.trace = None  # optional list: (stage, torch.cuda.Event) appended after each stage
+        self._lref = C.byref(self._raw)
+        self._h = None
+        self._create(int(max_sel_k))
+        self._timing = False
 
-    def _mark(self, name):
-        if self.trace is not None:
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record()
-            self.trace.append((name, ev))
+    # -- native context
+    def _create(self, max_sel_k: int):
+        lib = self._lib
+        self.max_sel_k = max_sel_k
+        flags = (L.OP_FORCE_SIMT if self.force_simt else 0) | (0 if self.bwd_workspace else L.OP_NO_DS_WORKSPACE)
+        desc = L.vsa_op_desc_t(self.B, self.H, self.d, self.top_k, max_sel_k, self.model_dim,
+                               L.VSA_BF16 if self.dtype == torch.bfloat16 else L.VSA_F32, int(self.pool),
+                               self.activation, 1 if self.adaptation else 0, 1 if self.raster else 0, flags)
+        nbytes = lib.vsa_op_memory_bytes(self._lref, C.byref(desc))
+        h = C.c_void_p()
+        if nbytes == 0:  # invalid descriptor: let create report the reference's message
+            check(lib.vsa_op_create(self._lref, C.byref(desc), None, 0, C.byref(h)))
+        self._destroy()
+        self._mem = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        check(lib.vsa_op_create(self._lref, C.byref(desc), C.c_void_p(self._mem.data_ptr()), nbytes, C.byref(h)))
+        self._h = h
+        self._views()
+
+    def _destroy(self):
+        if getattr(self, "_h", None) is not None:
+            self._lib.vsa_op_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self._destroy()
+        except Exception:
+            pass
+
+    def _bufs(self) -> L.vsa_op_buffers_t:
+        b = L.vsa_op_buffers_t()
+        check(self._lib.vsa_op_buffers(self._h, C.byref(b)))
+        return b
+
+    def _views(self):
+        b = self._bufs()
+        base = self._mem.data_ptr()
+        B, H, d, nc, Lp = self.B, self.H, self.d, self.layout.num_cubes, self.layout.seq_padded
+        kmax = max(self.top_k, self.max_sel_k)
+
+        def view(ptr, shape, dt):
+            if not ptr:
+                return None
+            n = 1
+            for x in shape:
+                n *= x
+            es = torch.tensor([], dtype=dt).element_size()
+            off = ptr - base
+            return self._mem[off:off + n * es].view(dt).view(shape)
+
+        f32, i32, dt = torch.float32, torch.int32, self.dtype
+        self.q_t, self.k_t, self.v_t = (view(p, (B, H, Lp, d), dt) for p in (b.q_t, b.k_t, b.v_t))
+        self.qc, self.kc, self.vc = (view(p, (B, H, nc, d), f32) for p in (b.qc, b.kc, b.vc))
+        self.ac = view(b.ac, (B, H, nc, nc), f32)
+        self.oc = view(b.oc_cube, (B, H, nc, d), f32)
+        self.sel = view(b.sel, (B, H, nc, self.top_k), i32)
+        self.selT_offs = view(b.selT_offs, (B * H, nc + 1), i32)
+        self.selT_idx = view(b.selT_idx, (B * H, nc * kmax), i32)
+        self.o_f = view(b.o_fine, (B, H, Lp, d), dt)
+        self.lse = view(b.lse, (B, H, Lp), f32)
+        self.dof = view(b.dof, (B, H, Lp, d), dt)
+        self.delta = view(b.delta, (B, H, Lp), f32)
+        self.doc = view(b.doc_cube, (B, H, nc, d), f32)
+        self.dqc, self.dkc, self.dvc = (view(p, (B, H, nc, d), f32) for p in (b.dqc, b.dkc, b.dvc))
+        self.gc, self.gf, self.dgc, self.dgf = (view(p, self.io_shape, dt) for p in (b.gc, b.gf, b.dgc, b.dgf))
+        self.fine_sel, self.fine_k = self.sel, self.top_k
+
+    # -- timing (native CUDA events between stages, no host gaps)
+    def timing(self, enable: bool = True):
+        check(self._lib.vsa_op_timing(self._h, 1 if enable else 0))
+        self._timing = enable
+
+    def stage_ms(self) -> dict:
+        """Mean device time per stage over the calls since ``timing(True)`` (one sync)."""
+        ms = (C.c_float * len(L.OP_STAGES))()
+        calls = (C.c_int32 * 2)()
+        check(self._lib.vsa_op_stage_ms(self._h, ms, calls))
+        out = {n: float(ms[i]) for i, n in enumerate(L.OP_STAGES)}
+        out["_calls"] = (int(calls[0]), int(calls[1]))
+        return out
 
     @property
     def seq_io(self) -> int:
@@ -411,16 +475,27 @@ class VsaOp:
         if not t.is_contiguous():
             raise ValueError(f"{name}: must be contiguous")
 
+    def _override(self, sel_override):
+        if sel_override is None:
+            return None, 0
+        if (not isinstance(sel_override, torch.Tensor) or sel_override.dtype != torch.int32 or not sel_override.is_cuda
+                or sel_override.dim() != 4 or not sel_override.is_contiguous()):
+            raise ValueError("BlockSelection: expected contiguous int32 [B, H, nc, k] on CUDA")
+        if tuple(sel_override.shape[:3]) != tuple(self.sel.shape[:3]):
+            raise ValueError("fine stage: selection does not match shapes")
+        k = int(sel_override.shape[3])
+        if not (1 <= k <= self.layout.num_cubes):
+            raise ValueError("BlockSelection: k must be in [1, num_cubes]")
+        if k > max(self.top_k, self.max_sel_k):  # grow the transposed-map capacity (control path)
+            self._create(k)
+        return _p(sel_override), k
+
     def forward(self, q, k, v, gc, gf=None, out=None, sel_override=None, check_inputs=True, before_fine=None):
         """vsa_forward (vsa.hpp:89-122) at attention level: gates are given.
 
         ``before_fine``: optional callable run after the coarse stage, before the
         fine kernel (the first reader of the gates) — e.g. to wait for a gate
         exchange that overlapped K1-K3."""
-        lib, lr, st = self._lib, self._lref, _stream()
-        B, H, d = self.B, self.H, self.d
-        bh = B * H
-        dt = L.VSA_BF16 if self.dtype == torch.bfloat16 else L.VSA_F32
         if check_inputs:
             for t, n in ((q, "q"), (k, "k"), (v, "v"), (gc, "gate_coarse")):
                 self._chk(t, n)
@@ -428,104 +503,108 @@ class VsaOp:
                 if gf is None:
                     raise ValueError("vsa_forward: missing fine gate")
                 self._chk(gf, "gate_fine")
-        if self.raster:
-            xr = (C.c_void_p * 3)(q.data_ptr(), k.data_ptr(), v.data_ptr())
-            xt = (C.c_void_p * 3)(self.q_t.data_ptr(), self.k_t.data_ptr(), self.v_t.data_ptr())
-            pl = (C.c_void_p * 3)(self.qc.data_ptr(), self.kc.data_ptr(), self.vc.data_ptr())
-            self._mark("start")
-            check(lib.vsa_tile_pool(lr, bh, d, dt, 3, xr, xt, pl, self.pool, st))
-            self._mark("tile_pool")
-            qt, kt, vt = self.q_t, self.k_t, self.v_t
-        else:
-            qt, kt, vt = q, k, v
-            self._mark("start")
-            for x, p in ((q, self.qc), (k, self.kc), (v, self.vc)):
-                check(lib.vsa_pool_tiled(lr, bh, d, dt, _p(x), _p(p), self.pool, st))
-            self._mark("tile_pool")
-        override = sel_override is not None
-        check(lib.vsa_coarse_forward(lr, bh, d, _p(self.qc), _p(self.kc), _p(self.vc), self.top_k, _p(self.ac),
-                                     _p(self.oc), _p(self.sel), None if override else _p(self.selT_offs),
-                                     None if override else _p(self.selT_idx), _p(self.bitmap), st))
-        self._mark("coarse_fwd")
-        if override:
-            validate_selection(sel_override, self.layout.num_cubes)
-            if sel_override.shape[:3] != self.sel.shape[:3]:
-                raise ValueError("fine stage: selection does not match shapes")
-            self.fine_sel, self.fine_k = sel_override, int(sel_override.shape[3])
-            if self.selT_idx.shape[1] < self.layout.num_cubes * self.fine_k:
-                self.selT_idx = torch.empty((bh, self.layout.num_cubes * self.fine_k), dtype=torch.int32,
-                                            device=q.device)
-            check(lib.vsa_selection_transpose(lr, bh, _p(sel_override), self.fine_k, _p(self.selT_offs),
-                                              _p(self.selT_idx), _p(self.bitmap), st))
-        else:
-            self.fine_sel, self.fine_k = self.sel, self.top_k
+        ov, ok = self._override(sel_override)
+        st = _stream()
+        check(self._lib.vsa_op_forward_coarse(self._h, _p(q), _p(k), _p(v), ov, ok, st))
+        self.fine_sel, self.fine_k = (sel_override, ok) if ov is not None else (self.sel, self.top_k)
         if out is None:
             out = torch.empty(self.io_shape, dtype=self.dtype, device=q.device)
         if before_fine is not None:
             before_fine()
-        flags = L.FINE_COMBINE | (L.FINE_UNTILE if self.raster else 0) | (L.FINE_ADAPTATION if self.adaptation else 0)
-        if self.force_simt:
-            flags |= L.FINE_FORCE_SIMT
-        check(lib.vsa_fine_forward(lr, bh, d, dt, _p(qt), _p(kt), _p(vt), _p(self.fine_sel), self.fine_k,
-                                   _p(self.o_f), _p(self.lse), None, _p(gc), _p(gf), _p(self.oc), flags, _p(out), st))
-        self._mark("fine_fwd")
-        self._gc, self._gf = gc, gf
-        self._qkv = (qt, kt, vt)
+        check(self._lib.vsa_op_forward_fine(self._h, _p(gc), _p(gf), _p(out), st))
+        self._fwd = (q, k, v, gc, gf)  # the caller's tensors the artifacts point into stay alive
         return out
+
+    def _ensure_workspace(self, device):
+        if not self.bwd_workspace:
+            return
+        wsb = self._lib.vsa_op_workspace_bytes(self._h, self.fine_k)
+        if self.ws is not None and self.ws.numel() >= wsb:
+            return
+        free, _ = torch.cuda.mem_get_info(device)
+        if wsb > 0.6 * free:  # e.g. the dense baseline at 14B (all cubes): dQ recomputes S / dP instead
+            self.ws = None
+            check(self._lib.vsa_op_set_workspace(self._h, None, 0))
+            return
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+        check(self._lib.vsa_op_set_workspace(self._h, _p(self.ws), wsb))
+
+    @property
+    def used_ds_workspace(self) -> bool:
+        """Whether the last backward took the dS-materialising path (else dQ recomputed S / dP)."""
+        return bool(self._bufs().bwd_used_workspace)
 
     def backward(self, dout, dq=None, dk=None, dv=None, dgc=None, dgf=None, check_inputs=True):
         """vsa_backward (vsa.hpp:129-189) at attention level -> (dq, dk, dv, dgc, dgf)."""
-        if self._gc is None:
+        if getattr(self, "_fwd", None) is None:
             raise ValueError("vsa_backward: missing or mismatched forward artifacts")
         if check_inputs:
             self._chk(dout, "dO")
-        lib, lr, st = self._lib, self._lref, _stream()
-        B, H, d = self.B, self.H, self.d
-        bh = B * H
-        dt = L.VSA_BF16 if self.dtype == torch.bfloat16 else L.VSA_F32
         mk = lambda: torch.empty(self.io_shape, dtype=self.dtype, device=dout.device)
         dq = mk() if dq is None else dq
         dk = mk() if dk is None else dk
         dv = mk() if dv is None else dv
         dgc = mk() if dgc is None else dgc
         dgf = mk() if dgf is None else dgf
-        raster = 1 if self.raster else 0
-        if self.raster and self.layout.seq_padded != self.layout.seq_len:
-            pass  # padded rows of dq/dk/dv are never written (dropped at untile)
-        check(lib.vsa_backward_prologue(lr, bh, d, dt, raster, _p(dout), _p(self._gc), _p(self._gf), _p(self.oc),
-                                        _p(self.o_f), 1 if self.adaptation else 0, _p(self.dof), _p(self.delta),
-                                        _p(self.doc), _p(dgc), _p(dgf), st))
-        self._mark("prologue")
-        check(lib.vsa_coarse_backward(lr, bh, d, _p(self.qc), _p(self.kc), _p(self.vc), _p(self.ac), _p(self.doc),
-                                      _p(self.dqc), _p(self.dkc), _p(self.dvc), _p(self.scratch), st))
-        self._mark("coarse_bwd")
-        mean = self.pool == POOL_MEAN
-        qt, kt, vt = self._qkv
-        flags = L.FINE_FORCE_SIMT if self.force_simt else 0
-        wsb = lib.vsa_fine_backward_workspace_bytes(lr, bh, self.fine_k) if self.bwd_workspace else 0
-        if wsb and (self.ws is None or self.ws.numel() < wsb):
-            free, _ = torch.cuda.mem_get_info(dout.device)
-            if wsb > 0.6 * free:  # e.g. the dense baseline at 14B (all cubes): dQ recomputes S / dP instead
-                wsb = 0
-            else:
-                self.ws = torch.empty(wsb, dtype=torch.uint8, device=dout.device)
-        check(lib.vsa_fine_backward(lr, bh, d, dt, _p(qt), _p(kt), _p(vt), _p(self.dof), _p(self.lse),
-                                    _p(self.delta), _p(self.fine_sel), self.fine_k, _p(self.selT_offs),
-                                    _p(self.selT_idx), _p(self.dqc) if mean else None, _p(self.dkc) if mean else None,
-                                    _p(self.dvc) if mean else None, raster, flags, _p(dq), _p(dk), _p(dv),
-                                    _p(self.ws) if wsb else None, wsb, st))
-        self._mark("fine_bwd")
-        if not mean:
-            for x, dc, g in ((qt, self.dqc, dq), (kt, self.dkc, dk), (vt, self.dvc, dv)):
-                check(lib.vsa_unpool_max_add(lr, bh, d, dt, _p(x), _p(dc), raster, _p(g), st))
-        if self.adaptation:
-            dgf.zero_()
+        self._ensure_workspace(dout.device)
+        check(self._lib.vsa_op_backward(self._h, _p(dout), _p(dq), _p(dk), _p(dv), _p(dgc), _p(dgf), _stream()))
         return dq, dk, dv, dgc, dgf
+
+    # -- the reference's vsa_forward / vsa_backward with hidden states (model_dim > 0)
+    def forward_hidden(self, hidden, params: "VsaParams", q, k, v, out=None, sel_override=None):
+        """vsa_forward (vsa.hpp:89-122): gate projection (tcgen05 GEMM) + the operator."""
+        if self.model_dim <= 0:
+            raise ValueError("vsa_forward: the operator was created without model_dim (gate projection)")
+        _check_hidden(hidden, self.B, self.seq_io, self.model_dim)
+        params.check(self.model_dim, self.H, self.d)
+        for t, n in ((q, "q"), (k, "k"), (v, "v")):
+            self._chk(t, n)
+        ov, ok = self._override(sel_override)
+        if out is None:
+            out = torch.empty(self.io_shape, dtype=self.dtype, device=q.device)
+        bias = _gate_bias(params)
+        check(self._lib.vsa_forward(self._h, _p(hidden), _p(params.gate_weight), _p(bias), _p(q), _p(k), _p(v), ov,
+                                    ok, _p(out), _stream()))
+        self.fine_sel, self.fine_k = (sel_override, ok) if ov is not None else (self.sel, self.top_k)
+        self._fwd = (q, k, v, hidden, bias)
+        return out
+
+    def backward_hidden(self, hidden, params: "VsaParams", dout, dq=None, dk=None, dv=None):
+        """vsa_backward (vsa.hpp:129-189): -> (dq, dk, dv, dhidden, dgate_weight, dgate_bias)."""
+        if self.model_dim <= 0:
+            raise ValueError("vsa_backward: the operator was created without model_dim (gate projection)")
+        if getattr(self, "_fwd", None) is None:
+            raise ValueError("vsa_backward: missing or mismatched forward artifacts")
+        _check_hidden(hidden, self.B, self.seq_io, self.model_dim)
+        self._chk(dout, "dO")
+        mk = lambda: torch.empty(self.io_shape, dtype=self.dtype, device=dout.device)
+        dq = mk() if dq is None else dq
+        dk = mk() if dk is None else dk
+        dv = mk() if dv is None else dv
+        dhidden = torch.empty_like(hidden)
+        dW = torch.empty(params.gate_weight.shape, dtype=torch.float32, device=dout.device)
+        bias = _gate_bias(params)
+        db = torch.empty(bias.shape, dtype=torch.float32, device=dout.device) if bias is not None else None
+        self._ensure_workspace(dout.device)
+        check(self._lib.vsa_backward(self._h, _p(hidden), _p(params.gate_weight), _p(dout), _p(dq), _p(dk), _p(dv),
+                                     _p(dhidden), _p(dW), _p(db), _stream()))
+        return dq, dk, dv, dhidden, dW, db
 
     @property
     def artifacts(self) -> CoarseArtifacts:
         return CoarseArtifacts(self.qc, self.kc, self.vc, self.ac, self.oc, self.sel, self.selT_offs, self.selT_idx,
                                self.pool, self.layout.cube_size)
+
+
+def _check_hidden(hidden, B, S, md):
+    """check_hidden (vsa.hpp:75-80)."""
+    _cuda4(hidden, "hidden")
+    if hidden.shape[1] != 1:
+        raise ValueError("vsa: hidden states are [batch, 1, seq, model_dim]")
+    if hidden.shape[0] != B or hidden.shape[2] != S or hidden.shape[3] != md:
+        raise ValueError("vsa: hidden states do not match Q/K/V shapes")
+    if hidden.dtype != torch.bfloat16:
+        raise ValueError("gates: bf16 CUDA hidden and gate_weight required")
 
 
 class VsaHostPipeline:
@@ -544,8 +623,12 @@ class VsaHostPipeline:
         chunks = max(1, min(chunks, units))
         self.bounds = [(units * i) // chunks for i in range(chunks + 1)]
         self.units, self.d, self.S, self.dtype = units, d, layout.seq_len, dtype
-        cmax = max(b - a for a, b in zip(self.bounds[:-1], self.bounds[1:]))
-        self.ops = [VsaOp(layout, 1, cmax, d, top_k, dtype=dtype, device=device, **op_kwargs) for _ in range(2)]
+        sizes = sorted({b - a for a, b in zip(self.bounds[:-1], self.bounds[1:])})
+        cmax = sizes[-1]
+        # one operator per (group size, buffer slot), built here with the caller's options:
+        # run() never allocates, and ragged groups compute the same operator
+        self.ops = {(c, s): VsaOp(layout, 1, c, d, top_k, dtype=dtype, device=device, **op_kwargs)
+                    for c in sizes for s in range(2)}
         e = lambda: torch.empty((1, cmax, self.S, d), dtype=dtype, device=device)
         self.din = [[e() for _ in range(6)] for _ in range(2)]
         self.dout = [[e() for _ in range(6)] for _ in range(2)]
@@ -582,26 +665,17 @@ class VsaHostPipeline:
             comp.wait_event(ev_fwd_in)
             if i >= 2:
                 comp.wait_event(ev_out[i - 2])                # slot's outputs drained
-            op = self.ops[slot]
-            if c == op.H:
-                op.forward(*di[:5], out=do[0], check_inputs=False)
-                ev_fwd = ev()
-                ev_fwd.record(comp)
-                with torch.cuda.stream(self.s_out):
-                    self.s_out.wait_event(ev_fwd)
-                    hout[0][a:b].copy_(do[0][0, :c], non_blocking=True)
-                comp.wait_event(ev_bwd_in)
-                op.backward(di[5], *do[1:], check_inputs=False)
-                first_out = 1
-            else:  # ragged last group: run on views of the right head count
-                comp.wait_event(ev_bwd_in)
-                sub = VsaOp(op.layout, 1, c, self.d, op.top_k, dtype=self.dtype, device=di[0].device)
-                v = lambda t: t[:, :c].contiguous()
-                o = sub.forward(*(v(t) for t in di[:5]))
-                g = sub.backward(v(di[5]))
-                for dst, src in zip(do, (o, *g)):
-                    dst[:, :c].copy_(src)
-                first_out = 0
+            op = self.ops[(c, slot)]
+            v = lambda t: t[:, :c]  # [1, cmax, S, d] -> [1, c, S, d]: a contiguous prefix view
+            op.forward(*(v(t) for t in di[:5]), out=v(do[0]), check_inputs=False)
+            ev_fwd = ev()
+            ev_fwd.record(comp)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(ev_fwd)
+                hout[0][a:b].copy_(do[0][0, :c], non_blocking=True)
+            comp.wait_event(ev_bwd_in)
+            op.backward(v(di[5]), *(v(t) for t in do[1:]), check_inputs=False)
+            first_out = 1
             ev_comp[i] = ev()
             ev_comp[i].record(comp)
             with torch.cuda.stream(self.s_out):
@@ -627,6 +701,26 @@ class VsaParams:
     pool: int = POOL_MEAN
     activation: int = GATE_IDENTITY
     adaptation: bool = False
+
+    @staticmethod
+    def random_init(model_dim: int, heads: int, head_dim: int, top_k: int, rng=None, device="cuda",
+                    dtype=torch.bfloat16) -> "VsaParams":
+        """VsaParams::random_init (vsa.hpp:25-32): Wg ~ N(0, 1/model_dim), no bias.
+        ``rng``: a numpy-compatible draw function f(rows, cols, std) -> array (e.g. the
+        oracle's mt19937_64 randn_matrix for identical draws); default torch.randn."""
+        std = 1.0 / float(model_dim) ** 0.5
+        if rng is None:
+            w = torch.randn((model_dim, 2 * heads * head_dim), device=device) * std
+        else:
+            w = torch.as_tensor(rng(model_dim, 2 * heads * head_dim, std), dtype=torch.float32).to(device)
+        return VsaParams(w.to(dtype).contiguous(), None, int(top_k))
+
+    @staticmethod
+    def adaptation_init(model_dim: int, heads: int, head_dim: int, num_cubes: int, device="cuda",
+                        dtype=torch.bfloat16) -> "VsaParams":
+        """VsaParams::adaptation_init (vsa.hpp:35-42): Wg = 0, k = all cubes, Gf == 1."""
+        return VsaParams(torch.zeros((model_dim, 2 * heads * head_dim), dtype=dtype, device=device), None,
+                         int(num_cubes), adaptation=True)
 
     def check(self, model_dim, heads, head_dim):
         if tuple(self.gate_weight.shape) != (model_dim, 2 * heads * head_dim):
@@ -740,3 +834,84 @@ def selection_accuracy_qk(layout: TileLayout, q: torch.Tensor, k: torch.Tensor, 
     acc = torch.empty((B, H), dtype=torch.float64, device=q.device)
     check(L.lib().vsa_selection_accuracy_from_lse(_p(lse_sel), _p(lse_all), B * H, S, _p(acc), _stream()))
     return acc
+
+
+# ----------------------------------------------------------------------------- vsa_forward / vsa_backward
+@dataclass
+class VsaOutput:
+    """VsaOutput (vsa.hpp:56-63): the output plus the forward artifacts, resident in the
+    operator context ``op`` (coarse artifacts, fine output / lse, gates, fine_sel)."""
+
+    out: torch.Tensor
+    op: VsaOp
+
+    @property
+    def coarse(self) -> CoarseArtifacts:
+        return self.op.artifacts
+
+    @property
+    def fine(self) -> FineResult:
+        return FineResult(self.op.o_f, None, self.op.lse.view(-1, self.op.layout.seq_padded))
+
+    @property
+    def gate_coarse(self) -> torch.Tensor:
+        return self.op.gc
+
+    @property
+    def gate_fine(self) -> torch.Tensor:
+        return self.op.gf
+
+    @property
+    def fine_sel(self) -> torch.Tensor:
+        return self.op.fine_sel
+
+
+@dataclass
+class VsaGrads:
+    """VsaGrads (vsa.hpp:65-71)."""
+
+    dq: torch.Tensor
+    dk: torch.Tensor
+    dv: torch.Tensor
+    dhidden: torch.Tensor
+    dgate_weight: torch.Tensor
+    dgate_bias: torch.Tensor | None
+
+
+def vsa_forward(layout: TileLayout, hidden, q, k, v, params: VsaParams, sel_override=None,
+                raster: bool = False) -> VsaOutput:
+    """vsa_forward (vsa.hpp:89-122): gate projection, coarse stage (+ top-k), fine stage on
+    the selection (or ``sel_override``), gated combine. Like the reference, q, k, v and
+    hidden are tile-ordered ([B,H,Lp,d], [B,1,Lp,md]); ``raster=True`` takes raster-ordered
+    tensors ([B,H,t*h*w,d], [B,1,t*h*w,md]) with the tiling fused into the kernels."""
+    for t, n in ((q, "q"), (k, "k"), (v, "v")):
+        _cuda4(t, n)
+    if not (q.shape == k.shape == v.shape) or not (q.dtype == k.dtype == v.dtype):
+        raise ValueError("attention: Q, K, V must share one shape")
+    B, H, S, d = q.shape
+    if S != (layout.seq_len if raster else layout.seq_padded):
+        raise ValueError("vsa: sequence length does not match layout")
+    _check_hidden(hidden, B, S, hidden.shape[3])
+    params.check(hidden.shape[3], H, d)
+    if not (1 <= params.top_k <= layout.num_cubes):
+        raise ValueError("coarse_forward_select: k must be in [1, num_cubes]")
+    op = VsaOp(layout, B, H, d, params.top_k, dtype=q.dtype, pool=params.pool, adaptation=params.adaptation,
+               raster=raster, device=q.device, model_dim=hidden.shape[3], activation=int(params.activation),
+               max_sel_k=0 if sel_override is None else int(sel_override.shape[3]))
+    out = op.forward_hidden(hidden, params, q, k, v, sel_override=sel_override)
+    return VsaOutput(out, op)
+
+
+def vsa_backward(layout: TileLayout, fwd: VsaOutput, hidden, q, k, v, params: VsaParams, dout) -> VsaGrads:
+    """vsa_backward (vsa.hpp:129-189): path split, gate gradients through the activation
+    and projection, coarse + fine attention gradients."""
+    if fwd is None or not isinstance(fwd, VsaOutput) or fwd.op is None:
+        raise ValueError("vsa_backward: missing or mismatched forward artifacts")
+    if dout.shape != q.shape:
+        raise ValueError("vsa_backward: dO shape mismatch")
+    op = fwd.op
+    if tuple(q.shape) != op.io_shape:
+        raise ValueError("vsa_backward: missing or mismatched forward artifacts")
+    params.check(hidden.shape[3], op.H, op.d)
+    dq, dk, dv, dh, dW, db = op.backward_hidden(hidden, params, dout)
+    return VsaGrads(dq, dk, dv, dh, dW, db)

@@ -205,7 +205,8 @@ int vsa_coarse_forward(const vsa_layout_t* L, int64_t bh, int64_t d, const float
   VSA_REQUIRE(qc && kc && vc && ac && oc_cube && sel && bh >= 1, "coarse_forward_select: null buffer");
   VSA_REQUIRE((selT_offs == nullptr) == (selT_idx == nullptr), "coarse_forward_select: selT_offs/selT_idx pair");
   VSA_REQUIRE(selT_offs == nullptr || bitmap_ws != nullptr, "coarse_forward_select: transposed map needs bitmap_ws");
-  VSA_REQUIRE(L->nc <= 16384, "coarse_forward_select: num_cubes > 16384 unsupported");
+  // softmax + top-k keeps 4 rows of nc + 256 words in shared memory (227 KB per CTA)
+  VSA_REQUIRE(L->nc <= 14080, "coarse_forward_select: num_cubes > 14080 unsupported");
   return launch_coarse_forward(*L, bh, d, qc, kc, vc, top_k, ac, oc_cube, sel, selT_offs, selT_idx, bitmap_ws,
                                as_stream(stream));
 }
@@ -239,6 +240,11 @@ int vsa_fine_forward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype
     VSA_REQUIRE(out && gc && oc_cube && (gf || (flags & VSA_FINE_ADAPTATION)), "combine: missing gates / Oc");
   if (flags & VSA_FINE_UNTILE) VSA_REQUIRE(out != nullptr, "untile: missing output");
   cudaStream_t st = as_stream(stream);
+  // bf16 runs on the tcgen05 kernels (64-token cubes, d in {64, 128}); the SIMT kernels
+  // serve fp32 and, only when asked for explicitly, bf16 shapes outside that set
+  if (dtype == VSA_BF16 && !(flags & VSA_FINE_FORCE_SIMT))
+    VSA_REQUIRE(sm100_fine_supported(*L, d, dtype),
+                "fine stage: bf16 needs 64-token cubes and head_dim 64 or 128 (VSA_FINE_FORCE_SIMT for the SIMT path)");
   if (!(flags & VSA_FINE_FORCE_SIMT) && sm100_fine_supported(*L, d, dtype))
     return launch_fine_forward_sm100(*L, bh, d, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube, flags,
                                      out, st);
@@ -286,6 +292,9 @@ int vsa_fine_backward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtyp
   VSA_REQUIRE(top_k >= 1 && top_k <= L->nc, "fine stage: selection does not match shapes");
   VSA_REQUIRE(d >= 1 && L->cube <= 128 && L->cube * d <= 8192, "fine stage: cube*head_dim > 8192 unsupported");
   cudaStream_t st = as_stream(stream);
+  if (dtype == VSA_BF16 && !(flags & VSA_FINE_FORCE_SIMT))
+    VSA_REQUIRE(sm100_fine_bwd_supported(*L, d, dtype),
+                "fine_backward: bf16 needs 64-token cubes and head_dim 64 or 128 (VSA_FINE_FORCE_SIMT for the SIMT path)");
   if (!(flags & VSA_FINE_FORCE_SIMT) && sm100_fine_bwd_supported(*L, d, dtype))
     return launch_fine_backward_sm100(*L, bh, d, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc,
                                       dvc, raster, dq, dk, dv, workspace, workspace_bytes, st);
@@ -305,6 +314,40 @@ int vsa_unpool_max_add(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dty
   VSA_REQUIRE(dtype_ok(dtype), "unpool: unknown dtype");
   VSA_REQUIRE(x_tiled && dxc && dx && bh >= 1 && d >= 1 && d <= 1024, "unpool: null buffer");
   return launch_unpool_max_add(*L, bh, d, dtype, x_tiled, dxc, raster, dx, as_stream(stream));
+}
+
+int vsa_coarse_backward_tokens(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const float* qc,
+                               const float* kc, const float* vc, const float* ac, int32_t pool_mode,
+                               const void* doc, const void* q_t, const void* k_t, const void* v_t, float* doc_cube,
+                               float* dqc, float* dkc, float* dvc, float* scratch, void* dq, void* dk, void* dv,
+                               void* stream) {
+  VSA_CHECKED(check_layout(L));
+  VSA_REQUIRE(dtype_ok(dtype), "coarse_backward: unknown dtype");
+  VSA_CHECKED(check_vec_dim(d, dtype));
+  VSA_REQUIRE(ac != nullptr, "coarse_backward: artifacts do not match layout");
+  VSA_REQUIRE(pool_mode == VSA_POOL_MEAN || pool_mode == VSA_POOL_MAX, "pool_cubes: unknown pool mode");
+  VSA_REQUIRE(qc && kc && vc && doc && doc_cube && dqc && dkc && dvc && scratch && dq && dk && dv && bh >= 1,
+              "coarse_backward: null buffer");
+  VSA_REQUIRE(pool_mode == VSA_POOL_MEAN || (q_t && k_t && v_t), "coarse_backward: max pooling needs q, k, v");
+  cudaStream_t st = as_stream(stream);
+  // dOc_cube = sum of dOc over each cube's tokens (coarse.hpp:146), sequential fp32 in tile order
+  const void* xs[1] = {doc};
+  float* pl[1] = {doc_cube};
+  VSA_CHECKED(launch_tile_pool(*L, bh, d, dtype, 1, xs, nullptr, pl, kPoolSum, 1, st));
+  VSA_CHECKED(launch_coarse_backward(*L, bh, d, qc, kc, vc, ac, doc_cube, dqc, dkc, dvc, scratch, st));
+  const float* dc[3] = {dqc, dkc, dvc};
+  void* gs[3] = {dq, dk, dv};
+  const void* xt[3] = {q_t, k_t, v_t};
+  for (int i = 0; i < 3; ++i) {
+    if (pool_mode == VSA_POOL_MEAN) {
+      VSA_CHECKED(launch_unpool_mean(*L, bh, d, dtype, dc[i], gs[i], st));
+    } else {
+      const size_t n = size_t(bh) * size_t(L->seq_padded) * size_t(d) * (dtype == VSA_BF16 ? 2 : 4);
+      VSA_CHECKED(cuda_status(cudaMemsetAsync(gs[i], 0, n, st), "coarse_backward: zero"));
+      VSA_CHECKED(launch_unpool_max_add(*L, bh, d, dtype, xt[i], dc[i], 0, gs[i], st));
+    }
+  }
+  return VSA_OK;
 }
 
 }  // extern "C"

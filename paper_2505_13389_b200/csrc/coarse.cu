@@ -286,6 +286,27 @@ __global__ void unpool_max_kernel(DevLayout L, int d, const T* __restrict__ x, c
   *p = from_f<T>(to_f(*p) + dxc[(u * L.nc + c) * d + j]);
 }
 
+// mean-pool unpool (coarse.hpp:164-168): every token of a cube gets dxc[cube] / cube.
+// Tiled output [bh, seqp, d]; one thread per 16-byte chunk.
+template <typename T>
+__global__ void unpool_mean_kernel(DevLayout L, int64_t bh, int d, const float* __restrict__ dxc, T* __restrict__ dx) {
+  constexpr int V = Vec<T>::N;
+  const int chunks = d / V;
+  const int64_t total = bh * L.seqp * chunks;
+  const float cube = float(L.cube);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = i / chunks;
+    const int ch = int(i - row * chunks);
+    const int64_t u = row / L.seqp;
+    const int c = int((row - u * L.seqp) / L.cube);
+    const float* src = dxc + (u * L.nc + c) * d + ch * V;
+    float v[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) v[j] = src[j] / cube;  // IEEE division, as the oracle
+    store16(dx + row * d + ch * V, v);
+  }
+}
+
 }  // namespace vsa_dev
 
 namespace vsa_host {
@@ -325,7 +346,10 @@ int launch_coarse_forward(const vsa_layout_t& L, int64_t bh, int64_t d, const fl
   {
     const int64_t rows = bh * nc;
     const size_t smem = 4 * (nc + 256) * sizeof(uint32_t);
-    cudaFuncSetAttribute(coarse_softmax_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int rc0 = cuda_status(
+        cudaFuncSetAttribute(coarse_softmax_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+        "coarse_softmax_topk_kernel: shared memory");
+    if (rc0) return rc0;
     coarse_softmax_topk_kernel<<<unsigned((rows + 3) / 4), 128, smem, st>>>(rows, nc, int(top_k), ac, sel, bitmap,
                                                                             words);
     int rc = kernel_status("coarse_softmax_topk_kernel");
@@ -398,6 +422,18 @@ int launch_unpool_max_add(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t 
     unpool_max_kernel<float><<<grid, thr, 0, st>>>(to_dev(L), int(d), static_cast<const float*>(x_tiled), dxc,
                                                    raster, static_cast<float*>(dx));
   VSA_LAUNCH_CHECK("unpool_max_kernel");
+}
+
+int launch_unpool_mean(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, const float* dxc, void* dx,
+                       cudaStream_t st) {
+  const int64_t total = bh * L.seq_padded * (d * (dtype == VSA_BF16 ? 2 : 4) / 16);
+  const unsigned blocks = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  if (dtype == VSA_BF16)
+    unpool_mean_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(to_dev(L), bh, int(d), dxc,
+                                                              static_cast<__nv_bfloat16*>(dx));
+  else
+    unpool_mean_kernel<float><<<blocks, 256, 0, st>>>(to_dev(L), bh, int(d), dxc, static_cast<float*>(dx));
+  VSA_LAUNCH_CHECK("unpool_mean_kernel");
 }
 
 }  // namespace vsa_host

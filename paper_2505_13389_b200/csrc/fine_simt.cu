@@ -280,9 +280,15 @@ __global__ void __launch_bounds__(kSimtThreads) fine_dkdv_simt_kernel(
 namespace vsa_host {
 using namespace vsa_dev;
 
+// Opt a SIMT kernel into `bytes` of dynamic shared memory; shapes whose tiles do not fit
+// the 227 KB per-CTA limit are rejected as invalid arguments (not a launch failure).
 template <typename K>
-static void set_smem(K kernel, size_t bytes) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+static int set_smem(K kernel, size_t bytes, const char* what) {
+  if (bytes > size_t(227) * 1024) {
+    set_error("%s: cube*head_dim too large for the SIMT kernels (%zu B of shared memory > 227 KB)", what, bytes);
+    return VSA_EINVAL;
+  }
+  return cuda_status(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)), what);
 }
 
 template <typename T>
@@ -291,7 +297,7 @@ static int fwd_t(const vsa_layout_t& Lh, int64_t bh, int64_t d, const void* q, c
                  const float* oc, int32_t flags, void* out, cudaStream_t st) {
   const int B = int(Lh.cube), D = int(d);
   const size_t smem = sizeof(float) * (size_t(B) * (D + 1) * 2 + size_t(B) * D + size_t(B) * (B + 1) + 3 * B);
-  set_smem(fine_fwd_simt_kernel<T>, smem);
+  if (int rc = set_smem(fine_fwd_simt_kernel<T>, smem, "fine_forward")) return rc;
   dim3 grid(unsigned(Lh.nc), unsigned(bh));
   fine_fwd_simt_kernel<T><<<grid, kSimtThreads, smem, st>>>(
       to_dev(Lh), D, int(top_k), 1.0f / std::sqrt(float(d)), static_cast<const T*>(q), static_cast<const T*>(k),
@@ -319,7 +325,7 @@ static int bwd_t(const vsa_layout_t& Lh, int64_t bh, int64_t d, const void* q, c
   dim3 grid(unsigned(Lh.nc), unsigned(bh));
   {
     const size_t smem = sizeof(float) * (size_t(B) * (D + 1) * 4 + size_t(B) * (B + 1) + 2 * B);
-    set_smem(fine_dq_simt_kernel<T>, smem);
+    if (int rc = set_smem(fine_dq_simt_kernel<T>, smem, "fine_backward")) return rc;
     fine_dq_simt_kernel<T><<<grid, kSimtThreads, smem, st>>>(
         to_dev(Lh), D, int(top_k), scale, static_cast<const T*>(q), static_cast<const T*>(k),
         static_cast<const T*>(v), static_cast<const T*>(dof), lse, delta, sel, dqc, raster, static_cast<T*>(dq));
@@ -328,7 +334,7 @@ static int bwd_t(const vsa_layout_t& Lh, int64_t bh, int64_t d, const void* q, c
   }
   {
     const size_t smem = sizeof(float) * (size_t(B) * (D + 1) * 4 + size_t(B) * (B + 1) * 2 + 2 * B);
-    set_smem(fine_dkdv_simt_kernel<T>, smem);
+    if (int rc = set_smem(fine_dkdv_simt_kernel<T>, smem, "fine_backward")) return rc;
     fine_dkdv_simt_kernel<T><<<grid, kSimtThreads, smem, st>>>(
         to_dev(Lh), D, int(top_k), scale, static_cast<const T*>(q), static_cast<const T*>(k),
         static_cast<const T*>(v), static_cast<const T*>(dof), lse, delta, offs, idx, dkc, dvc, raster,

@@ -28,6 +28,10 @@ int launch_gemm_f32_grouped(int ngroups, const GemmF32Args* args, int batch, cud
 // debug event trace target (vsa_debug_trace); buf == nullptr when disabled
 vsa_dev::TraceCfg debug_trace();
 
+// Internal pool mode of launch_tile_pool: the sequential fp32 sum over a cube's tokens
+// (tile order) without the division of the mean (the dOc cube sums of coarse_backward,
+// coarse.hpp:146).
+constexpr int32_t kPoolSum = 2;
 int launch_tile_pool(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, int32_t n, const void* const* xr,
                      void* const* xt, float* const* pooled, int32_t pool_mode, int in_tiled, cudaStream_t st);
 int launch_untile(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, const void* xt, void* x,
@@ -53,6 +57,8 @@ int launch_backward_prologue(const vsa_layout_t& L, int64_t bh, int64_t d, int32
 int launch_coarse_backward(const vsa_layout_t& L, int64_t bh, int64_t d, const float* qc, const float* kc,
                            const float* vc, const float* ac, const float* doc_cube, float* dqc, float* dkc,
                            float* dvc, float* scratch, cudaStream_t st);
+int launch_unpool_mean(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, const float* dxc, void* dx,
+                       cudaStream_t st);
 int launch_unpool_max_add(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dtype, const void* x_tiled,
                           const float* dxc, int32_t raster, void* dx, cudaStream_t st);
 

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
         if (xt) *reinterpret_cast<uint4*>(xt + (tile_base + o) * d + ch * V) = raw[b];
         float v[V];
         load16(reinterpret_cast<const T*>(&raw[b]), v);
-        if (pool_mode == VSA_POOL_MEAN) {
+        if (pool_mode != VSA_POOL_MAX) {  // mean, or the internal sum mode
 #pragma unroll
           for (int i = 0; i < V; ++i) acc[i] = acc[i] + v[i];
         } else {
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
           for (int i = 0; i < V; ++i) v[i] = 0.f;
         }
         if (xt) store16(xt + (tile_base + o) * d + ch * V, v);
-        if (pool_mode == VSA_POOL_MEAN) {
+        if (pool_mode != VSA_POOL_MAX) {  // mean, or the internal sum mode
 #pragma unroll
           for (int i = 0; i < V; ++i) acc[i] = acc[i] + v[i];
         } else {

@@ -55,7 +55,7 @@ class UlyssesExchange:
     """
 
     def __init__(self, B: int, S: int, H: int, d: int, group=None,
-                 transpose_blocks: Callable = transpose_blocks_cuda):
+                 transpose_blocks: Callable = transpose_blocks_cuda, host_staged: bool = False):
         self.group = group
         self.P = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         if H % self.P or S % self.P:
@@ -63,6 +63,18 @@ class UlyssesExchange:
         self.B, self.S, self.H, self.d = B, S, H, d
         self.Sc, self.Hl = S // self.P, H // self.P
         self.tb = transpose_blocks
+        # host_staged: the all-to-all runs on host copies (for a CPU-only process group, e.g.
+        # gloo with several ranks sharing one GPU in tests); the default exchanges the
+        # device buffers directly (NCCL over NVLink)
+        self.host_staged = host_staged
+
+    def _all_to_all(self, recv, send, async_op=False):
+        if not self.host_staged:
+            return dist.all_to_all_single(recv, send, group=self.group, async_op=async_op)
+        r = torch.empty(recv.shape, dtype=recv.dtype)
+        dist.all_to_all_single(r, send.cpu(), group=self.group)
+        recv.copy_(r)
+        return None
 
     @property
     def shard_shape(self):
@@ -89,7 +101,7 @@ class UlyssesExchange:
         recv = torch.empty(self.head_shape, dtype=x.dtype, device=x.device)
         send = torch.empty_like(recv)
         self.tb(x, send, self.B * self.Sc, self.P, self.Hl * self.d)
-        work = dist.all_to_all_single(recv, send, group=self.group, async_op=async_op)
+        work = self._all_to_all(recv, send, async_op=async_op)
         return (recv, work) if async_op else recv
 
     def to_seq(self, y: torch.Tensor) -> torch.Tensor:
@@ -98,7 +110,7 @@ class UlyssesExchange:
             return y.view(self.shard_shape)
         out = torch.empty(self.shard_shape, dtype=y.dtype, device=y.device)
         recv = torch.empty_like(y)
-        dist.all_to_all_single(recv, y, group=self.group)
+        self._all_to_all(recv, y)
         self.tb(recv, out, self.P, self.B * self.Sc, self.Hl * self.d)
         return out
 
@@ -109,10 +121,11 @@ class UlyssesVsa:
     Each rank runs VsaOp on H/P heads over the whole sequence, reading the
     all-to-all receive buffers in place (io="bshd", seq_chunks=P)."""
 
-    def __init__(self, layout, B: int, H: int, d: int, top_k: int, group=None, dtype=torch.bfloat16, **op_kwargs):
+    def __init__(self, layout, B: int, H: int, d: int, top_k: int, group=None, dtype=torch.bfloat16,
+                 host_staged: bool = False, **op_kwargs):
         from .api import VsaOp
 
-        self.x = UlyssesExchange(B, layout.seq_len, H, d, group)
+        self.x = UlyssesExchange(B, layout.seq_len, H, d, group, host_staged=host_staged)
         self.op = VsaOp(layout, B, self.x.Hl, d, top_k, dtype=dtype, io="bshd", seq_chunks=self.x.P, **op_kwargs)
 
     def forward(self, q, k, v, gc, gf=None) -> torch.Tensor:

@@ -135,6 +135,86 @@ int main() {
     }
     CHECK(worst <= 1.0, "bf16 fine_forward outside 2e-2 + 1e-2|ref| (ratio %.3f)", worst);
   }
+  // ---- vsa_forward / vsa_backward with hidden states and VsaParams (vsa.hpp:89-189)
+  {
+    const Index md = 256;
+    std::mt19937_64 r2(71);
+    auto qf = AttnTensor<float>::randn(B, H, S, d, r2);
+    auto kf = AttnTensor<float>::randn(B, H, S, d, r2);
+    auto vf = AttnTensor<float>::randn(B, H, S, d, r2);
+    auto hf = AttnTensor<float>::randn(B, 1, S, md, r2);
+    auto df = AttnTensor<float>::randn(B, H, S, d, r2);
+    auto tob = [](const AttnTensor<float>& x) {
+      AttnTensor<bf16> y(x.batch(), x.heads(), x.seq(), x.dim());
+      for (Index i = 0; i < x.size(); ++i) y.data()[i] = __float2bfloat16(x.data()[i]);
+      return y;
+    };
+    auto rnd = [](const AttnTensor<float>& x) {
+      AttnTensor<float> y(x.batch(), x.heads(), x.seq(), x.dim());
+      for (Index i = 0; i < x.size(); ++i) y.data()[i] = bfr(x.data()[i]);
+      return y;
+    };
+    const auto qb = tob(qf), kb = tob(kf), vb = tob(vf), hb = tob(hf), db = tob(df);
+    const auto qr = rnd(qf), kr = rnd(kf), vr = rnd(vf), dr = rnd(df);
+    // adaptation_init: Wg = 0, Gf = 1, k = nc -> the dense attention (test_vsa.cpp:32-52)
+    const auto pa = VsaParams<bf16>::adaptation_init(md, H, d, nc);
+    const auto fa = vsa_forward(L, hb, qb, kb, vb, pa);
+    const auto all = BlockSelection::all_cubes(B, H, nc);
+    std::vector<float> out(q.size()), rmax(B * H * S), lse(B * H * S);
+    orc_fine_forward_f32(la[0], la[1], la[2], la[3], la[4], la[5], qr.data(), kr.data(), vr.data(), B, H, S, d,
+                         all.data(), B, H, nc, nc, out.data(), rmax.data(), lse.data());
+    double worst = 0;
+    for (Index i = 0; i < q.size(); ++i)
+      worst = std::max(worst, std::fabs(__bfloat162float(fa.out.data()[i]) - out[i]) / (2e-2 + 1e-2 * std::fabs(out[i])));
+    CHECK(worst <= 1.0, "adaptation_init vsa_forward != dense attention (ratio %.3f)", worst);
+    const auto ga = vsa_backward(L, fa, hb, qb, kb, vb, pa, db);
+    std::vector<float> dq(q.size()), dk(q.size()), dv(q.size()), delta(B * H * S);
+    orc_fine_backward_f32(la[0], la[1], la[2], la[3], la[4], la[5], qr.data(), kr.data(), vr.data(), B, H, S, d,
+                          all.data(), B, H, nc, nc, dr.data(), lse.data(), dq.data(), dk.data(), dv.data(),
+                          delta.data());
+    // Gc = 0 in adaptation_init, so the coarse path contributes no Q/K/V gradient
+    double wq = 0, wk = 0, wv = 0;
+    for (Index i = 0; i < q.size(); ++i) {
+      wq = std::max(wq, std::fabs(__bfloat162float(ga.dq.data()[i]) - dq[i]) / (2e-2 + 1e-2 * std::fabs(dq[i])));
+      wk = std::max(wk, std::fabs(__bfloat162float(ga.dk.data()[i]) - dk[i]) / (2e-2 + 1e-2 * std::fabs(dk[i])));
+      wv = std::max(wv, std::fabs(__bfloat162float(ga.dv.data()[i]) - dv[i]) / (2e-2 + 1e-2 * std::fabs(dv[i])));
+    }
+    CHECK(wq <= 1.0 && wk <= 1.0 && wv <= 1.0, "adaptation vsa_backward != dense backward (%.3f %.3f %.3f)", wq, wk, wv);
+    const Index cols = 2 * H * d;
+    bool right_zero = true;
+    for (Index r = 0; r < md; ++r)
+      for (Index c = H * d; c < cols; ++c) right_zero &= ga.dgate_weight[size_t(r * cols + c)] == 0.f;
+    CHECK(right_zero, "adaptation: the fine half of dWg must be exactly 0");
+    // random_init (sigmoid): the output is the gated sum of the returned artifacts
+    auto pr = VsaParams<bf16>::random_init(md, H, d, k, r2);
+    pr.activation = GateActivation::kSigmoid;
+    const auto fr = vsa_forward(L, hb, qb, kb, vb, pr);
+    double wc = 0;
+    for (Index b = 0; b < B; ++b)
+      for (Index h = 0; h < H; ++h)
+        for (Index s = 0; s < S; ++s)
+          for (Index j = 0; j < d; ++j) {
+            const float oc = fr.coarse.oc_cube[size_t(((b * H + h) * nc + s / L.cube_size) * d + j)];
+            const float ref = oc * __bfloat162float(fr.gate_coarse.at(b, h, s, j)) +
+                              __bfloat162float(fr.fine.out.at(b, h, s, j)) * __bfloat162float(fr.gate_fine.at(b, h, s, j));
+            const float g = __bfloat162float(fr.out.at(b, h, s, j));
+            wc = std::max(wc, double(std::fabs(g - ref)) / (1e-2 + 1e-2 * std::fabs(ref)));
+          }
+    CHECK(wc <= 1.0, "vsa_forward out != Oc*Gc + Of*Gf of its artifacts (ratio %.3f)", wc);
+    bool sig_ok = true;
+    for (Index i = 0; i < fr.gate_coarse.size(); ++i) {
+      const float g = __bfloat162float(fr.gate_coarse.data()[i]);
+      sig_ok &= g > 0.f && g < 1.f;
+    }
+    CHECK(sig_ok, "sigmoid gates outside (0, 1)");
+    const auto gr = vsa_backward(L, fr, hb, qb, kb, vb, pr, db);
+    bool finite = true;
+    for (Index i = 0; i < gr.dhidden.size(); ++i) finite &= std::isfinite(__bfloat162float(gr.dhidden.data()[i]));
+    for (float x : gr.dgate_weight) finite &= std::isfinite(x);
+    CHECK(finite && gr.dhidden.dim() == md, "vsa_backward gate gradients");
+    CHECK(throws_invalid([&] { vsa_forward(L, hb, qb, kb, vb, VsaParams<bf16>::random_init(md + 64, H, d, k, r2)); }),
+          "mismatched gate projection must throw");
+  }
   // ---- invalid selections throw (test_fine.cpp:89-114)
   {
     BlockSelection bad(B, H, nc, 2);

@@ -89,3 +89,10 @@ def test_bench_reference_arm_runs_on_cpu():
     for k in ("metric", "value", "unit", "impl", "cpu_baseline", "e2e", "higher_is_better"):
         assert k in line, k
     assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "port"
+    # the driver pairs the two arms on the metric string: it must be the ours-arm string
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert line["metric"] == bench.metric_name(bench.CONFIGS["tiny"])
+    # ms_per_step x steps is what was timed (one head sample per step)
+    assert line["steps"] == 1 and line["ms_per_step"] > 0

@@ -39,5 +39,8 @@ def test_bench_line_has_every_contract_key():
 
 def test_reference_arm_line():
     d = run_bench("--impl", "reference", "--config", "tiny", "--steps", "1", "--warmup", "3")
+    ours = run_bench("--config", "tiny", "--steps", "3", "--warmup", "3", "--no-dense", "--no-cpu")
+    assert d["metric"] == ours["metric"] and d["unit"] == ours["unit"]
+    assert d["higher_is_better"] == ours["higher_is_better"]
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["value"] == d["value"]

@@ -1,6 +1,6 @@
 # SPDX-License-Identifier: Apache-2.0
-"""A/B helper: median per-stage device time over N steps of the Wan2.1-1.3B layer."""
-import statistics
+"""A/B helper: mean per-stage device time over N back-to-back steps of the Wan2.1-1.3B layer
+(native stage events, no host gaps)."""
 import sys
 
 import torch
@@ -17,14 +17,8 @@ for _ in range(3):
     op.forward(*x[:5])
     op.backward(x[5])
 torch.cuda.synchronize()
-acc = {}
+op.timing(True)
 for _ in range(n):
-    op.trace = []
     op.forward(*x[:5])
     op.backward(x[5])
-    torch.cuda.synchronize()
-    tr = op.trace
-    for (_, a), (name, b) in zip(tr[:-1], tr[1:]):
-        acc.setdefault(name, []).append(a.elapsed_time(b))
-    acc.setdefault("step", []).append(tr[0][1].elapsed_time(tr[-1][1]))
-print({k: round(statistics.median(v), 4) for k, v in acc.items()})
+print({k: round(v, 4) if isinstance(v, float) else v for k, v in op.stage_ms().items()})
