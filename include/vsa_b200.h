@@ -78,6 +78,11 @@ uint64_t vsa_kernel_launches(void);
  * instrumented kernels into the device buffer `buf` (uint64: [0] = count, then pairs);
  * buf = NULL disables. Not thread-safe; for profiling only. */
 int vsa_debug_trace(void* buf, int32_t cap, int32_t cta_x, int32_t cta_y);
+/* Debug: MacCounter on the device (tensor.hpp:36-39, fine.hpp:59-63). While set, every
+ * fine-forward launch atomically adds the number of (query cube, key cube) tiles its
+ * CTAs actually executed to *dev_counter (a device uint64); MACs = tiles * 2 * cube^2 * d.
+ * NULL disables. Process-global, not thread-safe; for instrumentation only. */
+int vsa_debug_tile_counter(uint64_t* dev_counter);
 
 /* Replaces: TileLayout::TileLayout (layout.cpp:6-31). VSA_PAD_REJECT reproduces
  * the reference's divisibility check (layout.cpp:10-11); VSA_PAD_ZERO rounds the

@@ -279,17 +279,24 @@ FineResult<Scalar> fine_forward(const TileLayout& layout, const AttnTensor<Scala
                                 const AttnTensor<Scalar>& v, const BlockSelection& sel, MacCounter* counter = nullptr) {
   detail::check_fine(layout, q, k, v, sel);
   const Index bh = q.batch() * q.heads(), d = q.dim(), n = q.size();
-  if (counter) {
-    counter->tiles += static_cast<std::uint64_t>(bh * layout.num_cubes * sel.k());
-    counter->macs += static_cast<std::uint64_t>(bh * layout.num_cubes * sel.k()) * 2ull * layout.cube_size *
-                     layout.cube_size * static_cast<std::uint64_t>(d);
-  }
   detail::DeviceBuffer<Scalar> dq(q.data(), n), dk(k.data(), n), dv(v.data(), n), dout(n);
   detail::DeviceBuffer<int32_t> dsel(sel.data(), static_cast<size_t>(bh * layout.num_cubes * sel.k()));
   detail::DeviceBuffer<float> lse(static_cast<size_t>(bh * q.seq())), rmax(static_cast<size_t>(bh * q.seq()));
-  detail::check(vsa_fine_forward(layout.raw(), bh, d, detail::dtype_of<Scalar>(), dq.get(), dk.get(), dv.get(),
-                                 dsel.get(), sel.k(), dout.get(), lse.get(), rmax.get(), nullptr, nullptr, nullptr, 0,
-                                 nullptr, nullptr));
+  // MacCounter (fine.hpp:59-63): the kernels count the tiles they execute on the device
+  const std::uint64_t zero = 0;
+  detail::DeviceBuffer<std::uint64_t> ctr(counter ? &zero : nullptr, counter ? 1 : 0);
+  if (counter) detail::check(vsa_debug_tile_counter(ctr.get()));
+  const int rc = vsa_fine_forward(layout.raw(), bh, d, detail::dtype_of<Scalar>(), dq.get(), dk.get(), dv.get(),
+                                  dsel.get(), sel.k(), dout.get(), lse.get(), rmax.get(), nullptr, nullptr, nullptr, 0,
+                                  nullptr, nullptr);
+  if (counter) vsa_debug_tile_counter(nullptr);
+  detail::check(rc);
+  if (counter) {
+    std::uint64_t tiles = 0;
+    ctr.to_host(&tiles);
+    counter->tiles += tiles;
+    counter->macs += tiles * 2ull * static_cast<std::uint64_t>(layout.cube_size * layout.cube_size * d);
+  }
   FineResult<Scalar> res{AttnTensor<Scalar>(q.batch(), q.heads(), q.seq(), d), {}};
   dout.to_host(res.out.data());
   res.saved.row_lse.resize(lse.size());

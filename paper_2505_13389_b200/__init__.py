@@ -11,6 +11,6 @@ from .api import (  # noqa: F401
     coarse_forward_select, coarse_from_pooled, fine_backward, fine_forward, flatten_index, gate_backward,
     gates_from_hidden, pool_cubes, selection_transpose, tile, tile_pool, untile, validate_selection,
     aggregate_probs_to_cubes, selection_accuracy, selection_accuracy_qk, VsaOutput, VsaGrads, vsa_forward,
-    vsa_backward, GATE_IDENTITY, GATE_SIGMOID,
+    vsa_backward, GATE_IDENTITY, GATE_SIGMOID, MacCounter,
 )
 from .ulysses import UlyssesExchange, UlyssesVsa, transpose_blocks_cuda  # noqa: F401,E402

@@ -46,7 +46,7 @@ OP_FORCE_SIMT, OP_NO_DS_WORKSPACE = 1, 2
 OP_STAGES = ["tile_pool", "coarse_fwd", "fine_fwd", "prologue", "coarse_bwd", "fine_bwd"]
 
 EXPORTS = [
-    "vsa_last_error", "vsa_version", "vsa_kernel_launches", "vsa_debug_trace", "vsa_layout_make", "vsa_flatten_index", "vsa_tile", "vsa_untile",
+    "vsa_last_error", "vsa_version", "vsa_kernel_launches", "vsa_debug_trace", "vsa_debug_tile_counter", "vsa_layout_make", "vsa_flatten_index", "vsa_tile", "vsa_untile",
     "vsa_tile_pool", "vsa_pool_tiled", "vsa_coarse_forward", "vsa_coarse_bitmap_bytes", "vsa_selection_transpose",
     "vsa_validate_selection", "vsa_fine_forward", "vsa_backward_prologue", "vsa_coarse_backward",
     "vsa_fine_backward", "vsa_fine_backward_workspace_bytes", "vsa_unpool_max_add", "vsa_layout_set_io",
@@ -89,6 +89,7 @@ def lib():
     sig = {
         "vsa_layout_make": [I64] * 6 + [I32, LP],
         "vsa_debug_trace": [P, I32, I32, I32],
+        "vsa_debug_tile_counter": [P],
         "vsa_layout_set_io": [LP, I32, I64, I64, I64],
         "vsa_transpose_blocks": [P, P, I64, I64, I64, P],
         "vsa_gate_forward": [LP, I64, I64, I64, I64, P, P, P, I32, I32, P, P, P],

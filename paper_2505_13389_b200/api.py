@@ -274,16 +274,39 @@ def _check_fine(layout, q, k, v, sel):
     validate_selection(sel, layout.num_cubes)
 
 
-def fine_forward(layout: TileLayout, q, k, v, sel, force_simt: bool = False) -> FineResult:
-    """fine_forward (fine.hpp:43-99) on tile-ordered q, k, v."""
+@dataclass
+class MacCounter:
+    """MacCounter (tensor.hpp:36-39): executed tiles and MACs, counted ON THE DEVICE by the
+    fine-forward kernels (vsa_debug_tile_counter); macs = tiles * 2 * cube^2 * d (fine.hpp:59-63)."""
+
+    tiles: int = 0
+    macs: int = 0
+
+
+def fine_forward(layout: TileLayout, q, k, v, sel, force_simt: bool = False,
+                 counter: MacCounter | None = None) -> FineResult:
+    """fine_forward (fine.hpp:43-99) on tile-ordered q, k, v. ``counter`` (debug) adds the
+    tiles the kernel executed, read back from a device counter (one sync)."""
     _check_fine(layout, q, k, v, sel)
     B, H, S, d = q.shape
     out = torch.empty_like(q)
     lse = torch.empty((B * H, S), dtype=torch.float32, device=q.device)
     rmax = torch.empty((B * H, S), dtype=torch.float32, device=q.device)
     flags = L.FINE_FORCE_SIMT if force_simt else 0
-    check(L.lib().vsa_fine_forward(layout.ref(), B * H, d, _dt(q), _p(q), _p(k), _p(v), _p(sel), sel.shape[3],
+    lib = L.lib()
+    ctr = torch.zeros(1, dtype=torch.int64, device=q.device) if counter is not None else None
+    if ctr is not None:
+        check(lib.vsa_debug_tile_counter(_p(ctr)))
+    try:
+        check(lib.vsa_fine_forward(layout.ref(), B * H, d, _dt(q), _p(q), _p(k), _p(v), _p(sel), sel.shape[3],
                                    _p(out), _p(lse), _p(rmax), None, None, None, flags, None, _stream()))
+    finally:
+        if ctr is not None:
+            lib.vsa_debug_tile_counter(None)
+    if ctr is not None:
+        tiles = int(ctr.item())
+        counter.tiles += tiles
+        counter.macs += tiles * 2 * layout.cube_size * layout.cube_size * d
     return FineResult(out, rmax, lse)
 
 

@@ -36,6 +36,9 @@ static vsa_dev::TraceCfg g_trace{nullptr, 0, 0, 0};
 
 vsa_dev::TraceCfg debug_trace() { return g_trace; }
 
+static unsigned long long* g_tile_ctr = nullptr;
+unsigned long long* debug_tile_counter() { return g_tile_ctr; }
+
 int kernel_status(const char* where) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError(), where);
@@ -87,6 +90,11 @@ uint64_t vsa_kernel_launches(void) { return g_launches.load(std::memory_order_re
 
 int vsa_debug_trace(void* buf, int32_t cap, int32_t cta_x, int32_t cta_y) {
   g_trace = vsa_dev::TraceCfg{static_cast<unsigned long long*>(buf), cap, cta_x, cta_y};
+  return VSA_OK;
+}
+
+int vsa_debug_tile_counter(uint64_t* dev_counter) {
+  g_tile_ctr = reinterpret_cast<unsigned long long*>(dev_counter);
   return VSA_OK;
 }
 

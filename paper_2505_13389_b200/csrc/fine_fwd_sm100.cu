@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                           float scale_log2, float tau, const int32_t* __restrict__ sel, __nv_bfloat16* __restrict__ of,
                           float* __restrict__ lse, float* __restrict__ rmax, const __nv_bfloat16* __restrict__ gc,
                           const __nv_bfloat16* __restrict__ gf, const float* __restrict__ oc, int flags,
-                          __nv_bfloat16* __restrict__ out, TraceCfg tr) {
+                          __nv_bfloat16* __restrict__ out, TraceCfg tr, unsigned long long* __restrict__ tile_ctr) {
   using C = FwdCfg<D>;
   constexpr int NG = C::kNG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       int item = 0;
+      unsigned long long tiles = 0;  // executed (query cube, key cube) tiles (MacCounter, fine.hpp:59-63)
       for (int j = 0; j < ntask_local; ++j) {
         const int t = int(blockIdx.x) + j * ncta;
         const int64_t u = t / L.nc;
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int ka = srow[2 * p];
           const bool hb = 2 * p + 1 < k_sel;
           const int kb = hb ? srow[2 * p + 1] : 0;
+          tiles += hb ? 2 : 1;
           for (int h = 0; h < 2; ++h, ++item) {
             const int g = item % NG;
             const CUtensorMap* tm = h ? &tm_v : &tm_k;
@@ -263,6 +265,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
         }
       }
+      if (tile_ctr) atomicAdd(tile_ctr, tiles);
     }
   } else if (warp == 14) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtl));
@@ -625,7 +628,8 @@ static int fwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
   kern<<<grid, kFwdThreads, smem, st>>>(tq, tk, tv, to_dev(Lh), int(ntasks), int(top_k), scale_log2, tau, sel,
                                        static_cast<__nv_bfloat16*>(o_fine), lse, row_max,
                                        static_cast<const __nv_bfloat16*>(gc), static_cast<const __nv_bfloat16*>(gf),
-                                       oc_cube, flags, static_cast<__nv_bfloat16*>(out), debug_trace());
+                                       oc_cube, flags, static_cast<__nv_bfloat16*>(out), debug_trace(),
+                                       debug_tile_counter());
   VSA_LAUNCH_CHECK("fine_fwd_sm100_kernel");
 }
 

@@ -40,8 +40,9 @@ __global__ void __launch_bounds__(kSimtThreads) fine_fwd_simt_kernel(
     DevLayout L, int d, int k, float scale, const T* __restrict__ q, const T* __restrict__ kk,
     const T* __restrict__ v, const int32_t* __restrict__ sel, T* __restrict__ of, float* __restrict__ lse,
     float* __restrict__ rmax, const T* __restrict__ gc, const T* __restrict__ gf, const float* __restrict__ oc,
-    int flags, T* __restrict__ out) {
+    int flags, T* __restrict__ out, unsigned long long* __restrict__ tile_ctr) {
   extern __shared__ float sm[];
+  if (tile_ctr && threadIdx.x == 0) atomicAdd(tile_ctr, static_cast<unsigned long long>(k));  // MacCounter
   const int B = L.cube, dp = d + 1, Bp = B + 1;
   float* Qs = sm;              // [B][d+1]
   float* Ks = Qs + B * dp;     // [B][d+1]
@@ -302,7 +303,7 @@ static int fwd_t(const vsa_layout_t& Lh, int64_t bh, int64_t d, const void* q, c
   fine_fwd_simt_kernel<T><<<grid, kSimtThreads, smem, st>>>(
       to_dev(Lh), D, int(top_k), 1.0f / std::sqrt(float(d)), static_cast<const T*>(q), static_cast<const T*>(k),
       static_cast<const T*>(v), sel, static_cast<T*>(of), lse, rmax, static_cast<const T*>(gc),
-      static_cast<const T*>(gf), oc, flags, static_cast<T*>(out));
+      static_cast<const T*>(gf), oc, flags, static_cast<T*>(out), debug_tile_counter());
   VSA_LAUNCH_CHECK("fine_fwd_simt_kernel");
 }
 

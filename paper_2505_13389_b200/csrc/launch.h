@@ -27,6 +27,8 @@ int launch_gemm_f32_grouped(int ngroups, const GemmF32Args* args, int batch, cud
 
 // debug event trace target (vsa_debug_trace); buf == nullptr when disabled
 vsa_dev::TraceCfg debug_trace();
+// debug tile counter of the fine forward kernels (vsa_debug_tile_counter); nullptr when disabled
+unsigned long long* debug_tile_counter();
 
 // Internal pool mode of launch_tile_pool: the sequential fp32 sum over a cube's tokens
 // (tile order) without the division of the mean (the dOc cube sums of coarse_backward,
