@@ -34,7 +34,12 @@ extern "C" {
 enum { VSA_OK = 0, VSA_EINVAL = -1 };
 enum { VSA_F32 = 0, VSA_BF16 = 1 };
 enum { VSA_POOL_MEAN = 0, VSA_POOL_MAX = 1 };            /* PoolMode, coarse.hpp:13 */
-enum { VSA_PAD_REJECT = 0, VSA_PAD_ZERO = 1 };           /* layout.cpp:10-11 rejects; ZERO = extension */
+/* layout.cpp:10-11 rejects non-divisible grids; the two pad modes are extensions:
+ * ZERO: the grid is padded with zero tokens that are ordinary tokens (pooled, attendable) — the
+ *       reference run on the padded layout (parity mode);
+ * MASK: FastVideo-style — padded keys are excluded from attention (-inf), cube means / maxima are
+ *       over the valid tokens only, the mean unpool divides by the valid count. */
+enum { VSA_PAD_REJECT = 0, VSA_PAD_ZERO = 1, VSA_PAD_MASK = 2 };
 enum { VSA_GATE_IDENTITY = 0, VSA_GATE_SIGMOID = 1 };    /* GateActivation, vsa.hpp:9 */
 /* Raster I/O order of the raster-ordered tensors (q, k, v, gates, out, dO, grads).
  * HEAD_MAJOR: [B, H, S, d] (AttnTensor, tensor.hpp:44-123).

@@ -17,7 +17,7 @@ CSRC = os.path.join(_PKG, "csrc")
 
 VSA_F32, VSA_BF16 = 0, 1
 POOL_MEAN, POOL_MAX = 0, 1
-PAD_REJECT, PAD_ZERO = 0, 1
+PAD_REJECT, PAD_ZERO, PAD_MASK = 0, 1, 2
 FINE_COMBINE, FINE_UNTILE, FINE_ADAPTATION, FINE_FORCE_SIMT = 1, 2, 4, 8
 IO_HEAD_MAJOR, IO_SEQ_MAJOR = 0, 1
 

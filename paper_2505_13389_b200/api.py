@@ -52,13 +52,18 @@ def _cuda4(t: torch.Tensor, name: str) -> None:
 
 # ----------------------------------------------------------------------------- layout
 class TileLayout:
-    """vsa::TileLayout (layout.hpp:14-33). ``pad=True`` enables the zero-pad
-    extension for non-divisible grids (the reference rejects them, layout.cpp:10-11)."""
+    """vsa::TileLayout (layout.hpp:14-33). The reference rejects non-divisible grids
+    (layout.cpp:10-11); ``pad=True`` (or ``"zero"``) pads with zero tokens that are ordinary
+    tokens (the parity mode), ``pad="mask"`` pads FastVideo-style: padded keys are excluded
+    from attention and cube means / maxima are over the real tokens."""
 
     def __init__(self, tokens_t, tokens_h, tokens_w, cube_t=4, cube_h=4, cube_w=4, pad=False):
+        modes = {False: L.PAD_REJECT, None: L.PAD_REJECT, True: L.PAD_ZERO, "zero": L.PAD_ZERO, "mask": L.PAD_MASK}
+        if pad not in modes:
+            raise ValueError("TileLayout: pad must be False, True / 'zero' or 'mask'")
         self._raw = L.vsa_layout_t()
-        check(L.lib().vsa_layout_make(tokens_t, tokens_h, tokens_w, cube_t, cube_h, cube_w,
-                                      L.PAD_ZERO if pad else L.PAD_REJECT, C.byref(self._raw)))
+        check(L.lib().vsa_layout_make(tokens_t, tokens_h, tokens_w, cube_t, cube_h, cube_w, modes[pad],
+                                      C.byref(self._raw)))
 
     def ref(self):
         return C.byref(self._raw)
@@ -77,6 +82,7 @@ class TileLayout:
     seq_len = property(lambda s: s._raw.seq)            # raster tokens
     seq_padded = property(lambda s: s._raw.seq_padded)  # tiled tokens (== seq_len unless padded)
     padded = property(lambda s: (s._raw.tp, s._raw.hp, s._raw.wp))
+    mask_pad = property(lambda s: s._raw.pad_mode == L.PAD_MASK)
 
     def __repr__(self):
         r = self._raw

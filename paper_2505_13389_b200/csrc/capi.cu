@@ -103,7 +103,8 @@ int vsa_layout_make(int64_t t, int64_t h, int64_t w, int64_t ct, int64_t ch, int
   VSA_REQUIRE(out != nullptr, "TileLayout: null output");
   VSA_REQUIRE(t >= 1 && h >= 1 && w >= 1, "TileLayout: token extents must be >= 1");
   VSA_REQUIRE(ct >= 1 && ch >= 1 && cw >= 1, "TileLayout: cube extents must be >= 1");
-  VSA_REQUIRE(pad_mode == VSA_PAD_REJECT || pad_mode == VSA_PAD_ZERO, "TileLayout: unknown pad mode");
+  VSA_REQUIRE(pad_mode == VSA_PAD_REJECT || pad_mode == VSA_PAD_ZERO || pad_mode == VSA_PAD_MASK,
+              "TileLayout: unknown pad mode");
   if (pad_mode == VSA_PAD_REJECT)
     VSA_REQUIRE(t % ct == 0 && h % ch == 0 && w % cw == 0,
                 "TileLayout: token extents must be integer multiples of cube extents");

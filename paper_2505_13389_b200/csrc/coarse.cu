@@ -268,11 +268,12 @@ __global__ void unpool_max_kernel(DevLayout L, int d, const T* __restrict__ x, c
   const int c = blockIdx.x, j = threadIdx.x;
   if (j >= d) return;
   const int64_t base = u * L.seqp + int64_t(c) * L.cube;
-  int am = 0;
-  float best = to_f(x[base * d + j]);
-  for (int t = 1; t < L.cube; ++t) {
+  int am = -1;
+  float best = 0.f;
+  for (int t = 0; t < L.cube; ++t) {
+    if (L.mask && !tile_token_valid(L, c, t)) continue;  // mask pad: argmax over real tokens
     const float v = to_f(x[(base + t) * d + j]);
-    if (v > best) { best = v; am = t; }
+    if (am < 0 || v > best) { best = v; am = t; }
   }
   int64_t row;
   if (raster) {
@@ -293,16 +294,18 @@ __global__ void unpool_mean_kernel(DevLayout L, int64_t bh, int d, const float* 
   constexpr int V = Vec<T>::N;
   const int chunks = d / V;
   const int64_t total = bh * L.seqp * chunks;
-  const float cube = float(L.cube);
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t row = i / chunks;
     const int ch = int(i - row * chunks);
     const int64_t u = row / L.seqp;
     const int c = int((row - u * L.seqp) / L.cube);
+    const float cube = pool_divisor(L, c);
+    const int off = int(row - u * L.seqp - int64_t(c) * L.cube);
+    const bool real = !L.mask || tile_token_valid(L, c, off);  // mask pad: padded tokens get 0
     const float* src = dxc + (u * L.nc + c) * d + ch * V;
     float v[V];
 #pragma unroll
-    for (int j = 0; j < V; ++j) v[j] = src[j] / cube;  // IEEE division, as the oracle
+    for (int j = 0; j < V; ++j) v[j] = real ? src[j] / cube : 0.f;  // IEEE division, as the oracle
     store16(dx + row * d + ch * V, v);
   }
 }

@@ -23,6 +23,7 @@ struct DevLayout {
   int64_t seqp;    // nc*cube
   // raster I/O order (vsa_layout_set_io): 0 = [B,H,S,d]; 1 = [S/chunk][B][chunk][H][d]
   int io;
+  int mask;  // VSA_PAD_MASK: padded tokens are excluded (keys at -inf, means over valid tokens)
   int64_t io_batch, io_heads, io_chunk;
 };
 
@@ -34,6 +35,7 @@ inline DevLayout to_dev(const vsa_layout_t& L) {
   d.cube = int(L.cube); d.nc = int(L.nc);
   d.seq = L.seq; d.seqp = L.seq_padded;
   d.io = int(L.io_order);
+  d.mask = L.pad_mode == VSA_PAD_MASK ? 1 : 0;
   d.io_batch = L.io_batch; d.io_heads = L.io_heads; d.io_chunk = L.io_chunk;
   return d;
 }
@@ -60,6 +62,32 @@ __host__ __device__ __forceinline__ int64_t raster_of_tile(const DevLayout& L, i
   const int t = ci * L.ct + oi, h = cj * L.ch + oj, w = ck * L.cw + ok;
   if (t >= L.t || h >= L.h || w >= L.w) return -1;
   return (int64_t(t) * L.h + h) * L.w + w;
+}
+
+// Whether token `off` of cube `c` is a real (non-padded) token.
+__host__ __device__ __forceinline__ bool tile_token_valid(const DevLayout& L, int c, int off) {
+  return raster_of_tile(L, int64_t(c) * L.cube + off) >= 0;
+}
+
+// Number of real tokens of cube c (== cube unless the cube overlaps the padding).
+__host__ __device__ __forceinline__ int cube_valid_count(const DevLayout& L, int c) {
+  const int plane = L.nh * L.nw;
+  const int ci = c / plane, rem = c - ci * plane, cj = rem / L.nw, ck = rem - cj * L.nw;
+  auto clampc = [](int e, int rest) { return rest < 0 ? 0 : (rest < e ? rest : e); };
+  return clampc(L.ct, L.t - ci * L.ct) * clampc(L.ch, L.h - cj * L.ch) * clampc(L.cw, L.w - ck * L.cw);
+}
+
+// Divisor of the mean pool / unpool of cube c: the cube size, or its valid count in mask mode.
+__host__ __device__ __forceinline__ float pool_divisor(const DevLayout& L, int c) {
+  return float(L.mask ? cube_valid_count(L, c) : L.cube);
+}
+
+// 64-bit validity mask of the tokens of cube c (bit o = token o is real); cube <= 64.
+__device__ __forceinline__ uint64_t cube_token_mask(const DevLayout& L, int c) {
+  uint64_t m = 0;
+  for (int o = 0; o < L.cube; ++o)
+    if (tile_token_valid(L, c, o)) m |= uint64_t(1) << o;
+  return m;
 }
 
 template <typename T>

@@ -111,7 +111,7 @@ __device__ __forceinline__ void write_rows(const DevLayout& L, int64_t u, int cu
                                            const float* __restrict__ xc, int raster, __nv_bfloat16* __restrict__ dst,
                                            int tid, int nthr) {
   constexpr int CH = D / 8;
-  const float inv = 1.0f / float(L.cube);
+  const float div = pool_divisor(L, cube);  // mean unpool (mask pad: the cube's real tokens)
   for (int task = tid; task < 64 * CH; task += nthr) {
     const int r = task / CH, ch = task - r * CH;
     float v[8];
@@ -120,7 +120,7 @@ __device__ __forceinline__ void write_rows(const DevLayout& L, int64_t u, int cu
     if (xc) {
       const float* c = xc + (u * L.nc + cube) * D + ch * 8;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] += c[i] * inv;
+      for (int i = 0; i < 8; ++i) v[i] += c[i] / div;
     }
     int64_t row = u * L.seqp + int64_t(cube) * 64 + r;
     if (raster) {
@@ -503,14 +503,14 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     // mean-unpool term; the whole epilogue overlaps the next task's products.
     const int dl = (warp & 3) * 32 + lane;
     const uint32_t lrow = tbase + (uint32_t((warp & 3) * 32) << 16);
-    const float inv = 1.0f / float(L.cube);
     int acn = 0;
     for (int j = 0;; ++j) {
       const int t = next_task_warp(j);
       if (t < 0) break;
       const Task T = task(t);
       const int64_t o = (T.u * L.nc + T.kc) * D + dl;
-      const float xk = (dkc && dl < D) ? dkc[o] * inv : 0.f, xv = (dvc && dl < D) ? dvc[o] * inv : 0.f;
+      const float div = pool_divisor(L, T.kc);  // mean unpool (mask pad: the cube's real tokens)
+      const float xk = (dkc && dl < D) ? dkc[o] / div : 0.f, xv = (dvc && dl < D) ? dvc[o] / div : 0.f;
       // output rows of tokens lane and lane + 32 of the cube (-1: pad token)
       const int64_t r0 = cube_out_row(L, T.u, T.kc, lane, raster), r1 = cube_out_row(L, T.u, T.kc, lane + 32, raster);
       const bool acc = T.npairs > 0;
@@ -580,6 +580,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       };
       float nl2, ndl;
       row_stats(0, nl2, ndl);
+      // mask pad: validity of this warp's 32 key columns of the task's key cube
+      const uint32_t kmask = L.mask ? uint32_t(cube_token_mask(L, T.kc) >> (ch * 32)) : 0xffffffffu;
       for (int p = 0; p < T.npairs; ++p, ++P) {
         const int cq_g = gseq.next(2 * P), co_g = gseq.next(2 * P + 1);
         const uint32_t cq_par = (uses >> cq_g) & 1u;
@@ -609,6 +611,11 @@ __global__ void __launch_bounds__(kKVThreads, 1)
                       a, c);
             pf[2 * jj] = valid ? ex2b(a) : 0.f;
             pf[2 * jj + 1] = valid ? ex2b(c) : 0.f;
+          }
+          if (kmask != 0xffffffffu) {  // mask pad: P = 0 on padded keys (dS follows)
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj)
+              if (!((kmask >> jj) & 1u)) pf[jj] = 0.f;
           }
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) pk[jj] = pack_bf16(pf[2 * jj], pf[2 * jj + 1]);
@@ -1036,7 +1043,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&sm->s_free[g]);
-      if (!valid) {
+      // mask pad: this lane's key is a padded token -> P = 0, dS = 0
+      const bool kreal = !L.mask || (valid && tile_token_valid(L, srow[2 * p + (kl >> 6)], kl & 63));
+      if (!valid || !kreal) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) pd[j] = 0u;
       }

@@ -366,12 +366,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int j = 0; j < ntask_local; ++j) {
       const int tb = j & 1;
       const uint32_t tO = lrow + 128 + tb * 64 + qb0;
+      // mask pad: the key cubes of this query cube's pairs (for the padded-key test)
+      const int32_t* mrow_sel = nullptr;
+      if (L.mask) {
+        const int t = int(blockIdx.x) + j * ncta;
+        mrow_sel = sel + int64_t(t) * k_sel;  // t = u * nc + qc
+      }
 #pragma unroll
       for (int i = 0; i < 32; ++i) lsum[i] = 0.f;
       for (int p = 0; p < np; ++p, ++gp) {
         const int b = gp & 1;
         const uint32_t tS = lrow + b * 64 + qb0;
         const bool valid = kl < 64 || (2 * p + 1 < k_sel);
+        // mask pad: this lane's key is a padded token -> excluded (score -inf)
+        const bool kpad = mrow_sel != nullptr && valid && !tile_token_valid(L, mrow_sel[2 * p + (kl >> 6)], kl & 63);
         mbar_wait_sleep(&sm->s_full[b], (gp >> 1) & 1);
         if (threadIdx.x == 0) trace_ev(tr, 7, gp);
         tc_fence_after();
@@ -384,6 +392,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           f2_unpack(ffma2(f2(x[i], x[i + 1]), f2(scale_log2, scale_log2), f2(-mreg[i], -mreg[i + 1])), x[i], x[i + 1]);
           mx = fmaxf(mx, fmaxf(x[i], x[i + 1]));
         }
+        if (kpad) {
+          mx = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = -INFINITY;
+        }
         const bool upd = named_bar_or(barSoft, 128, valid && mx > tau);  // `valid` is warp-uniform
         if (threadIdx.x == 0) trace_ev(tr, 10, gp);
         if (upd) {
@@ -391,7 +404,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (valid) {
             tmem_ld32(tS, x);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] *= scale_log2;
+            for (int i = 0; i < 32; ++i) x[i] = kpad ? -INFINITY : x[i] * scale_log2;
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) x[i] = -INFINITY;
@@ -442,7 +455,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (valid) {
             tmem_ld32(tS, x);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = fmaf(x[i], scale_log2, -mreg[i]);
+            for (int i = 0; i < 32; ++i) x[i] = kpad ? -INFINITY : fmaf(x[i], scale_log2, -mreg[i]);
           }
         }
         // P^T buffer gp&1 was last read by O(gp-2), issued before S(gp): s_full(gp)

@@ -69,9 +69,11 @@ __global__ void __launch_bounds__(kSimtThreads) fine_fwd_simt_kernel(
     load_tile(Ks, dp, kk + kbase * d, B, d);
     load_tile(Vs, d, v + kbase * d, B, d);
     __syncthreads();
+    const int kcube = srow[t];
     for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
       const int i = e / B, j = e - i * B;
-      S[i * Bp + j] = dotf(Qs + i * dp, Ks + j * dp, d) * scale;
+      // mask pad: padded keys are excluded (score -inf, probability 0)
+      S[i * Bp + j] = (L.mask && !tile_token_valid(L, kcube, j)) ? -INFINITY : dotf(Qs + i * dp, Ks + j * dp, d) * scale;
     }
     __syncthreads();
     for (int i = threadIdx.x; i < B; i += blockDim.x) {
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(kSimtThreads) fine_fwd_simt_kernel(
 template <typename T>
 __device__ __forceinline__ void store_grad(const DevLayout& L, int64_t u, int cube_idx, int i, int c, int d,
                                            float val, const float* __restrict__ dxc, int raster, T* __restrict__ dx) {
-  if (dxc) val += dxc[(u * L.nc + cube_idx) * d + c] / float(L.cube);
+  if (dxc) val += dxc[(u * L.nc + cube_idx) * d + c] / pool_divisor(L, cube_idx);
   int64_t row = u * L.seqp + int64_t(cube_idx) * L.cube + i;
   if (raster) {
     const int64_t rr = raster_of_tile(L, int64_t(cube_idx) * L.cube + i);
@@ -179,9 +181,11 @@ __global__ void __launch_bounds__(kSimtThreads) fine_dq_simt_kernel(
     load_tile(Ks, dp, kk + kbase * d, B, d);
     load_tile(Vs, dp, v + kbase * d, B, d);
     __syncthreads();
+    const int kcube = srow[t];
     for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
       const int i = e / B, j = e - i * B;
-      const float p = expf(dotf(Qs + i * dp, Ks + j * dp, d) * scale - ls[i]);
+      const bool real = !L.mask || tile_token_valid(L, kcube, j);  // mask pad: P = 0 on padded keys
+      const float p = real ? expf(dotf(Qs + i * dp, Ks + j * dp, d) * scale - ls[i]) : 0.f;
       const float dpv = dotf(dOs + i * dp, Vs + j * dp, d);
       P[i * Bp + j] = p * (dpv - dl[i]) * scale;
     }
@@ -245,7 +249,8 @@ __global__ void __launch_bounds__(kSimtThreads) fine_dkdv_simt_kernel(
     __syncthreads();
     for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
       const int i = e / B, j = e - i * B;
-      const float p = expf(dotf(Qs + i * dp, Ks + j * dp, d) * scale - ls[i]);
+      const bool real = !L.mask || tile_token_valid(L, kc, j);  // mask pad: P = 0 on padded keys
+      const float p = real ? expf(dotf(Qs + i * dp, Ks + j * dp, d) * scale - ls[i]) : 0.f;
       const float dpv = dotf(dOs + i * dp, Vs + j * dp, d);
       P[i * Bp + j] = p;
       dS[i * Bp + j] = p * (dpv - dl[i]) * scale;

@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
 #pragma unroll
   for (int i = 0; i < V; ++i) acc[i] = 0.f;
   const int64_t tile_base = u * L.seqp + int64_t(c) * L.cube;
+  bool first = true;  // first pooled token (max pool starts from it)
   if (L.cube % 8 == 0) {
     // 8 tokens per batch, loads issued before use (memory-level parallelism); same
     // per-channel order of the pooled sum (tile order)
@@ -73,13 +74,15 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
         if (xt) *reinterpret_cast<uint4*>(xt + (tile_base + o) * d + ch * V) = raw[b];
         float v[V];
         load16(reinterpret_cast<const T*>(&raw[b]), v);
+        if (L.mask && !tile_token_valid(L, c, o)) continue;  // mask pad: padded tokens are not pooled
         if (pool_mode != VSA_POOL_MAX) {  // mean, or the internal sum mode
 #pragma unroll
           for (int i = 0; i < V; ++i) acc[i] = acc[i] + v[i];
         } else {
 #pragma unroll
-          for (int i = 0; i < V; ++i) acc[i] = (o == 0) ? v[i] : fmaxf_ordered(acc[i], v[i]);
+          for (int i = 0; i < V; ++i) acc[i] = first ? v[i] : fmaxf_ordered(acc[i], v[i]);
         }
+        first = false;
       }
     }
   } else {
@@ -99,20 +102,22 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
           for (int i = 0; i < V; ++i) v[i] = 0.f;
         }
         if (xt) store16(xt + (tile_base + o) * d + ch * V, v);
+        if (L.mask && !tile_token_valid(L, c, o)) continue;
         if (pool_mode != VSA_POOL_MAX) {  // mean, or the internal sum mode
 #pragma unroll
           for (int i = 0; i < V; ++i) acc[i] = acc[i] + v[i];
         } else {
 #pragma unroll
-          for (int i = 0; i < V; ++i) acc[i] = (o == 0) ? v[i] : fmaxf_ordered(acc[i], v[i]);
+          for (int i = 0; i < V; ++i) acc[i] = first ? v[i] : fmaxf_ordered(acc[i], v[i]);
         }
+        first = false;
       }
   }
   if (pooled) {
     if (pool_mode == VSA_POOL_MEAN) {
-      const float inv = float(L.cube);
+      const float div = pool_divisor(L, c);  // cube size (mask pad: its valid tokens)
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] = acc[i] / inv;
+      for (int i = 0; i < V; ++i) acc[i] = acc[i] / div;
     }
     float* dst = pooled + (u * L.nc + c) * d + ch * V;
 #pragma unroll
