@@ -57,9 +57,13 @@ __device__ __forceinline__ float ex2b(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// (No FMA-pipe exp offload here, unlike the forward: the compute warps share SMSPs
-// with the MMA-issuing warp, and the extra FMA-pipe instructions slowed the dK/dV
-// pass by ~10% — the issuer is more sensitive to issue-slot pressure than MUFU.)
+// FMA-pipe exp offload for half of the exponentials (VSA_BWD_POLY_EXP): off by default
+// at d = 128 (the compute warps share SMSPs with the MMA-issuing warp, and the extra
+// FMA-pipe instructions slowed the dK/dV pass by ~10%).
+#ifndef VSA_BWD_POLY_EXP
+#define VSA_BWD_POLY_EXP 0
+#endif
+constexpr bool kBwdPolyExp = VSA_BWD_POLY_EXP != 0;
 __device__ __forceinline__ void named_bar_b(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -610,7 +614,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
                             f2(scale_log2, scale_log2), f2(-lse2, -lse2)),
                       a, c);
             pf[2 * jj] = valid ? ex2b(a) : 0.f;
-            pf[2 * jj + 1] = valid ? ex2b(c) : 0.f;
+            pf[2 * jj + 1] = valid ? (kBwdPolyExp ? ex2_poly(c) : ex2b(c)) : 0.f;
           }
           if (kmask != 0xffffffffu) {  // mask pad: P = 0 on padded keys (dS follows)
 #pragma unroll

@@ -96,21 +96,10 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA/ALU pipes (FA4-style MUFU offload): round-to-nearest split
-// x = n + f, f in [-0.5, 0.5], degree-3 fit of 2^f (max rel. error 7.7e-5, far
-// below the bf16 rounding of P), 2^n added into the exponent field. Inputs are
-// clamped at -120 (2^-120 ~ 0 next to the running max's 2^0).
 #ifndef VSA_FWD_POLY_EXP
 #define VSA_FWD_POLY_EXP 0
 #endif
 constexpr bool kPolyExp = VSA_FWD_POLY_EXP != 0;
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -120.f);
-  const float t = x + 12582912.f;  // 1.5 * 2^23: rint(x) in the low mantissa bits
-  const float f = x - (t - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.05508872f, f, 0.24260436f), f, 0.6932763f), f, 0.99992895f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
 
 // bar.sync that also ORs a predicate across the participating threads (no smem)
 __device__ __forceinline__ bool named_bar_or(int id, int n, bool pred) {
