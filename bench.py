@@ -188,7 +188,7 @@ def run_ours(args, rank, world, local_rank):
     parts = partition_units(units, world)
     u0, u1 = parts[rank]
     n = u1 - u0
-    op = vsa.VsaOp(L, 1, n, d, K, dtype=dtype) if n else None
+    op = vsa.VsaOp(L, 1, n, d, K, dtype=dtype, coarse=args.coarse) if n else None
     q, k, v, gc, gf, do = make_inputs(cfg, S, dtype, dev, u0, u1)
     outs = [torch.empty_like(q) for _ in range(6)]
 
@@ -235,6 +235,34 @@ def run_ours(args, rank, world, local_rank):
     if op is not None:
         stage_ms = op.stage_ms()
         op.timing(False)
+
+    # the other coarse mode (fp32 canonical <-> bf16 tcgen05), same inputs: step and coarse times
+    other_coarse = None
+    if op is not None and world == 1 and L.num_cubes % 8 == 0:
+        alt = "bf16" if args.coarse == "fp32" else "fp32"
+        opa = vsa.VsaOp(L, 1, n, d, K, dtype=dtype, coarse=alt)
+
+        def astep():
+            opa.forward(q, k, v, gc, gf, out=outs[0], check_inputs=False)
+            opa.backward(do, *outs[1:], check_inputs=False)
+
+        for _ in range(2):
+            astep()
+        barrier()
+        opa.timing(True)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        na = max(3, min(args.steps, 10))
+        a0.record(st)
+        for _ in range(na):
+            astep()
+        a1.record(st)
+        barrier()
+        ast = opa.stage_ms()
+        ams = a0.elapsed_time(a1) / na
+        other_coarse = {"coarse": alt, "ms_per_step": round(ams, 4),
+                        "value": round(fl["total"] / (ams * 1e-3) / 1e12, 2),
+                        "stages_ms": {s_: round(ast[s_], 4) for s_ in STAGES}}
+        del opa
 
     # dense baseline: the same kernels with top-k = all cubes
     dense = None
@@ -395,6 +423,8 @@ def run_ours(args, rank, world, local_rank):
                              "(profiles/ncu_r1d_kernels.json, DESIGN.md section 4)"},
         "stages": stages,
         "dense_baseline": dense,
+        "coarse_mode": args.coarse,
+        "other_coarse_mode": other_coarse,
         "gate_projection": gate,
         "e2e": {"value": round(fl["total"] / (ems * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                 "ms_per_step": round(ems, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -608,6 +638,8 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=12, help="host-pipeline unit groups for the e2e leg")
+    ap.add_argument("--coarse", default="fp32", choices=["fp32", "bf16"],
+                    help="coarse-stage mode of the headline op: fp32 (bit-exact block map) or bf16 (tcgen05)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -137,6 +137,24 @@ int vsa_coarse_forward(const vsa_layout_t* layout, int64_t bh, int64_t d, const 
                        int32_t* selT_idx, void* bitmap_ws, void* stream);
 size_t vsa_coarse_bitmap_bytes(const vsa_layout_t* layout, int64_t bh);
 
+/* Coarse-stage precision (north_star kernel 3 / H3):
+ * VSA_COARSE_F32 : canonical fp32 order on the SIMT pipes — probabilities and the block map
+ *                  bit-exact with the reference's top-k (the parity mode, default);
+ * VSA_COARSE_BF16: the coarse products on the tensor cores (tcgen05, TMEM accumulators, TMA)
+ *                  from bf16 copies of the pooled cubes, the same fused softmax + top-k +
+ *                  transposed-map kernel; the map can differ where bf16 moves a score across
+ *                  the top-k boundary (validated by feeding the fine stage the oracle's map).
+ * The bf16 mode needs nc % 8 == 0 and a workspace of vsa_coarse_workspace_bytes(); it keeps
+ * bf16 Qc/Kc/Vc/P there for vsa_coarse_backward_ex. */
+enum { VSA_COARSE_F32 = 0, VSA_COARSE_BF16 = 1 };
+size_t vsa_coarse_workspace_bytes(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t precision);
+int vsa_coarse_forward_ex(const vsa_layout_t* layout, int64_t bh, int64_t d, const float* qc, const float* kc,
+                          const float* vc, int64_t top_k, int32_t precision, float* ac, float* oc_cube, int32_t* sel,
+                          int32_t* selT_offs, int32_t* selT_idx, void* bitmap_ws, void* coarse_ws, void* stream);
+int vsa_coarse_backward_ex(const vsa_layout_t* layout, int64_t bh, int64_t d, const float* qc, const float* kc,
+                           const float* vc, const float* ac, const float* doc_cube, float* dqc, float* dkc, float* dvc,
+                           float* scratch, int32_t precision, void* coarse_ws, void* stream);
+
 /* Builds the transposed CSR map from a user-supplied block map (e.g. the
  * sel_override of vsa.hpp:93,115, or random_selection / all_cubes). */
 int vsa_selection_transpose(const vsa_layout_t* layout, int64_t bh, const int32_t* sel, int64_t top_k,
@@ -267,6 +285,7 @@ typedef struct vsa_op_desc_t {
   int32_t adaptation;  /* VsaParams::adaptation (vsa.hpp:23): Gf == 1 */
   int32_t raster;      /* 1: q/k/v/gates/out/dO/grads raster-ordered (tiling fused); 0: tile-ordered (vsa.hpp:86) */
   int32_t flags;       /* VSA_OP_* */
+  int32_t coarse;      /* VSA_COARSE_F32 (bit-exact map, default) or VSA_COARSE_BF16 (tcgen05) */
 } vsa_op_desc_t;
 
 /* Device pointers of the context's buffers (views for callers and tests). */

@@ -31,7 +31,7 @@ class vsa_layout_t(C.Structure):
 
 class vsa_op_desc_t(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("batch", "heads", "head_dim", "top_k", "max_sel_k", "model_dim")] + [
-        (n, C.c_int32) for n in ("dtype", "pool_mode", "activation", "adaptation", "raster", "flags")]
+        (n, C.c_int32) for n in ("dtype", "pool_mode", "activation", "adaptation", "raster", "flags", "coarse")]
 
 
 class vsa_op_buffers_t(C.Structure):
@@ -43,6 +43,7 @@ class vsa_op_buffers_t(C.Structure):
 
 
 OP_FORCE_SIMT, OP_NO_DS_WORKSPACE = 1, 2
+COARSE_F32, COARSE_BF16 = 0, 1
 OP_STAGES = ["tile_pool", "coarse_fwd", "fine_fwd", "prologue", "coarse_bwd", "fine_bwd"]
 
 EXPORTS = [
@@ -55,6 +56,7 @@ EXPORTS = [
     "vsa_op_memory_bytes", "vsa_op_create", "vsa_op_destroy", "vsa_op_buffers", "vsa_op_set_workspace",
     "vsa_op_workspace_bytes", "vsa_op_forward", "vsa_op_forward_coarse", "vsa_op_forward_fine", "vsa_op_backward",
     "vsa_forward", "vsa_backward", "vsa_op_timing", "vsa_op_stage_ms", "vsa_coarse_backward_tokens",
+    "vsa_coarse_workspace_bytes", "vsa_coarse_forward_ex", "vsa_coarse_backward_ex",
 ]
 
 
@@ -124,6 +126,8 @@ def lib():
         "vsa_backward": [P, P, P, P, P, P, P, P, P, P, P],
         "vsa_op_timing": [P, I32],
         "vsa_op_stage_ms": [P, C.POINTER(C.c_float), C.POINTER(I32)],
+        "vsa_coarse_forward_ex": [LP, I64, I64, P, P, P, I64, I32, P, P, P, P, P, P, P, P],
+        "vsa_coarse_backward_ex": [LP, I64, I64, P, P, P, P, P, P, P, P, P, I32, P, P],
         "vsa_coarse_backward_tokens": [LP, I64, I64, I32, P, P, P, P, I32, P, P, P, P, P, P, P, P, P, P, P, P, P],
     }
     for name, args in sig.items():
@@ -137,6 +141,8 @@ def lib():
     L.vsa_gate_backward_workspace_bytes.restype = C.c_size_t
     L.vsa_op_memory_bytes.argtypes = [LP, C.POINTER(vsa_op_desc_t)]
     L.vsa_op_memory_bytes.restype = C.c_size_t
+    L.vsa_coarse_workspace_bytes.argtypes = [LP, I64, I64, I32]
+    L.vsa_coarse_workspace_bytes.restype = C.c_size_t
     L.vsa_op_workspace_bytes.argtypes = [P, I64]
     L.vsa_op_workspace_bytes.restype = C.c_size_t
     _lib = L

@@ -369,12 +369,18 @@ class VsaOp:
     Ulysses receive layout [P, B, S/P, H, d] (§8e) — consumed in place, no copies.
     ``model_dim > 0`` adds the gate projection (``forward_hidden`` / ``backward_hidden``,
     the reference's vsa_forward / vsa_backward with hidden states and VsaParams).
+    ``coarse="bf16"`` runs the coarse products on the tensor cores (tcgen05; the block map
+    may differ from the reference's near the top-k boundary); the default ``"fp32"`` is
+    the canonical-order mode whose map is bit-exact with the reference.
     """
 
     def __init__(self, layout: TileLayout, B: int, H: int, d: int, top_k: int, dtype=torch.bfloat16,
                  pool: int = POOL_MEAN, adaptation: bool = False, raster: bool = True, device="cuda",
                  force_simt: bool = False, bwd_workspace: bool = True, io: str = "bhsd", seq_chunks: int = 1,
-                 max_sel_k: int = 0, model_dim: int = 0, activation: int = GATE_IDENTITY):
+                 max_sel_k: int = 0, model_dim: int = 0, activation: int = GATE_IDENTITY, coarse: str = "fp32"):
+        if coarse not in ("fp32", "bf16"):
+            raise ValueError("coarse must be 'fp32' (bit-exact block map) or 'bf16' (tcgen05)")
+        self.coarse = coarse
         if not (1 <= top_k <= layout.num_cubes):
             raise ValueError("coarse_forward_select: k must be in [1, num_cubes]")
         if io not in ("bhsd", "bshd"):
@@ -415,7 +421,8 @@ class VsaOp:
         flags = (L.OP_FORCE_SIMT if self.force_simt else 0) | (0 if self.bwd_workspace else L.OP_NO_DS_WORKSPACE)
         desc = L.vsa_op_desc_t(self.B, self.H, self.d, self.top_k, max_sel_k, self.model_dim,
                                L.VSA_BF16 if self.dtype == torch.bfloat16 else L.VSA_F32, int(self.pool),
-                               self.activation, 1 if self.adaptation else 0, 1 if self.raster else 0, flags)
+                               self.activation, 1 if self.adaptation else 0, 1 if self.raster else 0, flags,
+                               L.COARSE_BF16 if self.coarse == "bf16" else L.COARSE_F32)
         nbytes = lib.vsa_op_memory_bytes(self._lref, C.byref(desc))
         h = C.c_void_p()
         if nbytes == 0:  # invalid descriptor: let create report the reference's message

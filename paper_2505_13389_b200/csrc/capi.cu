@@ -220,6 +220,44 @@ int vsa_coarse_forward(const vsa_layout_t* L, int64_t bh, int64_t d, const float
                                as_stream(stream));
 }
 
+size_t vsa_coarse_workspace_bytes(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t precision) {
+  if (!L || bh < 1 || d < 1 || precision != VSA_COARSE_BF16) return 0;
+  return coarse_bf16_ws_bytes(*L, bh, d);
+}
+
+int vsa_coarse_forward_ex(const vsa_layout_t* L, int64_t bh, int64_t d, const float* qc, const float* kc,
+                          const float* vc, int64_t top_k, int32_t precision, float* ac, float* oc_cube, int32_t* sel,
+                          int32_t* selT_offs, int32_t* selT_idx, void* bitmap_ws, void* coarse_ws, void* stream) {
+  VSA_REQUIRE(precision == VSA_COARSE_F32 || precision == VSA_COARSE_BF16, "coarse: unknown precision");
+  if (precision == VSA_COARSE_F32)
+    return vsa_coarse_forward(L, bh, d, qc, kc, vc, top_k, ac, oc_cube, sel, selT_offs, selT_idx, bitmap_ws, stream);
+  VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
+  VSA_REQUIRE(top_k >= 1 && top_k <= L->nc, "coarse_forward_select: k must be in [1, num_cubes]");
+  VSA_REQUIRE(d >= 8 && d % 8 == 0 && d <= 256, "coarse (bf16): head_dim must be a multiple of 8 in [8, 256]");
+  VSA_REQUIRE(L->nc % 8 == 0, "coarse (bf16): num_cubes must be a multiple of 8 (use the fp32 coarse mode)");
+  VSA_REQUIRE(L->nc <= 14080, "coarse_forward_select: num_cubes > 14080 unsupported");
+  VSA_REQUIRE(qc && kc && vc && ac && oc_cube && sel && coarse_ws && bh >= 1, "coarse_forward_select: null buffer");
+  VSA_REQUIRE((selT_offs == nullptr) == (selT_idx == nullptr), "coarse_forward_select: selT_offs/selT_idx pair");
+  VSA_REQUIRE(selT_offs == nullptr || bitmap_ws != nullptr, "coarse_forward_select: transposed map needs bitmap_ws");
+  return launch_coarse_forward_bf16(*L, bh, d, qc, kc, vc, top_k, ac, oc_cube, sel, selT_offs, selT_idx, bitmap_ws,
+                                    coarse_ws, as_stream(stream));
+}
+
+int vsa_coarse_backward_ex(const vsa_layout_t* L, int64_t bh, int64_t d, const float* qc, const float* kc,
+                           const float* vc, const float* ac, const float* doc_cube, float* dqc, float* dkc, float* dvc,
+                           float* scratch, int32_t precision, void* coarse_ws, void* stream) {
+  VSA_REQUIRE(precision == VSA_COARSE_F32 || precision == VSA_COARSE_BF16, "coarse: unknown precision");
+  if (precision == VSA_COARSE_F32)
+    return vsa_coarse_backward(L, bh, d, qc, kc, vc, ac, doc_cube, dqc, dkc, dvc, scratch, stream);
+  VSA_CHECKED(check_layout(L));
+  VSA_CHECKED(check_io(L, bh));
+  VSA_REQUIRE(ac != nullptr && coarse_ws != nullptr, "coarse_backward: artifacts do not match layout");
+  VSA_REQUIRE(d >= 8 && d % 8 == 0 && d <= 256 && L->nc % 8 == 0, "coarse (bf16): unsupported shape");
+  VSA_REQUIRE(doc_cube && dqc && dkc && dvc && scratch && bh >= 1, "coarse_backward: null buffer");
+  return launch_coarse_backward_bf16(*L, bh, d, ac, doc_cube, dqc, dkc, dvc, scratch, coarse_ws, as_stream(stream));
+}
+
 int vsa_selection_transpose(const vsa_layout_t* L, int64_t bh, const int32_t* sel, int64_t top_k,
                             int32_t* selT_offs, int32_t* selT_idx, void* bitmap_ws, void* stream) {
   VSA_CHECKED(check_layout(L));

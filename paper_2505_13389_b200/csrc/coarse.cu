@@ -56,7 +56,8 @@ __device__ __forceinline__ float canon_expf(float x) { return __double2float_rn(
 // One warp per (b,h,row). Dynamic smem per warp: nc floats + 256-bin histogram.
 __global__ void __launch_bounds__(128) coarse_softmax_topk_kernel(int64_t rows, int nc, int k,
                                                                    float* __restrict__ ac, int32_t* __restrict__ sel,
-                                                                   uint32_t* __restrict__ bitmap, int words) {
+                                                                   uint32_t* __restrict__ bitmap, int words,
+                                                                   __nv_bfloat16* __restrict__ pbf) {
   extern __shared__ uint32_t smu[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(128) coarse_softmax_topk_kernel(int64_t rows, 
     const float p = __fdiv_rn(fv[j], sum);
     fv[j] = p;
     arow[j] = p;
+    if (pbf) pbf[row * nc + j] = __float2bfloat16_rn(p);  // tcgen05 mode: the A operand of Oc = P Vc
   }
   __syncwarp();
 
@@ -102,9 +104,16 @@ __global__ void __launch_bounds__(128) coarse_softmax_topk_kernel(int64_t rows, 
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int b = lane; b < 256; b += 32) hist[b] = 0;
     __syncwarp();
-    for (int j = lane; j < nc; j += 32) {
-      const uint32_t b = vals[j];
-      if ((b & mask) == prefix) atomicAdd(&hist[(b >> shift) & 255u], 1u);
+    // warp-aggregated histogram: probabilities of one row share most high bits (the first
+    // passes put nearly every element in one bin), so lanes with equal bins are grouped with
+    // match.any and one leader adds the group size (no 32-way serialised shared atomics)
+    for (int base = 0; base < nc; base += 32) {
+      const int j = base + lane;
+      const uint32_t b = j < nc ? vals[j] : 0u;
+      const bool act = j < nc && (b & mask) == prefix;
+      const uint32_t key = act ? ((b >> shift) & 255u) : 0x100u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, key);
+      if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[key], uint32_t(__popc(peers)));
     }
     __syncwarp();
     // lane l owns bins [255-8l .. 248-8l] (descending); suffix counts from the top
@@ -247,7 +256,8 @@ __global__ void validate_sel_kernel(const int32_t* __restrict__ sel, int64_t row
 // --------------------------------------------------------------------------- coarse backward (cube level)
 // dS = Ac .* (dP - delta) * scale, delta_i = sum_j Ac_ij dP_ij (coarse.hpp:155-157). One warp per row, in place.
 __global__ void __launch_bounds__(128) coarse_bwd_ds_kernel(int64_t rows, int nc, float scale,
-                                                             const float* __restrict__ ac, float* __restrict__ ds) {
+                                                             const float* __restrict__ ac, float* __restrict__ ds,
+                                                             __nv_bfloat16* __restrict__ dsbf) {
   const int64_t row = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -257,7 +267,22 @@ __global__ void __launch_bounds__(128) coarse_bwd_ds_kernel(int64_t rows, int nc
   for (int j = lane; j < nc; j += 32) part = __fmaf_rn(a[j], r[j], part);
 #pragma unroll
   for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-  for (int j = lane; j < nc; j += 32) r[j] = a[j] * (r[j] - part) * scale;
+  for (int j = lane; j < nc; j += 32) {
+    const float v = a[j] * (r[j] - part) * scale;
+    r[j] = v;
+    if (dsbf) dsbf[row * nc + j] = __float2bfloat16_rn(v);
+  }
+}
+
+// fp32 -> bf16 copies of up to three same-size tensors (the tcgen05 coarse operands)
+__global__ void cast_bf16_kernel(int64_t n, const float* __restrict__ x0, const float* __restrict__ x1,
+                                 const float* __restrict__ x2, __nv_bfloat16* __restrict__ y0,
+                                 __nv_bfloat16* __restrict__ y1, __nv_bfloat16* __restrict__ y2) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    y0[i] = __float2bfloat16_rn(x0[i]);
+    if (x1) y1[i] = __float2bfloat16_rn(x1[i]);
+    if (x2) y2[i] = __float2bfloat16_rn(x2[i]);
+  }
 }
 
 // max-pool unpool: route dxc to the first argmax token per (cube, channel). grid (nc, bh), block d.
@@ -354,7 +379,7 @@ int launch_coarse_forward(const vsa_layout_t& L, int64_t bh, int64_t d, const fl
         "coarse_softmax_topk_kernel: shared memory");
     if (rc0) return rc0;
     coarse_softmax_topk_kernel<<<unsigned((rows + 3) / 4), 128, smem, st>>>(rows, nc, int(top_k), ac, sel, bitmap,
-                                                                            words);
+                                                                            words, nullptr);
     int rc = kernel_status("coarse_softmax_topk_kernel");
     if (rc) return rc;
   }
@@ -401,7 +426,7 @@ int launch_coarse_backward(const vsa_layout_t& L, int64_t bh, int64_t d, const f
   int rc = launch_gemm_f32(B, nc, nc, D, doc_cube, snd, D, 1, vc, snd, 1, D, scratch, snn, nc, nullptr, st);
   if (rc) return rc;
   // dS = Ac .* (dP - rowsum(Ac .* dP)) * scale  (in place)
-  coarse_bwd_ds_kernel<<<unsigned((bh * nc + 3) / 4), 128, 0, st>>>(bh * nc, nc, scale, ac, scratch);
+  coarse_bwd_ds_kernel<<<unsigned((bh * nc + 3) / 4), 128, 0, st>>>(bh * nc, nc, scale, ac, scratch, nullptr);
   rc = kernel_status("coarse_bwd_ds_kernel");
   if (rc) return rc;
   // dQc = dS Kc, dKc = dS^T Qc, dVc = Ac^T dOc: one grouped launch (3 x 240 tiles at 1.3B)
@@ -437,6 +462,91 @@ int launch_unpool_mean(const vsa_layout_t& L, int64_t bh, int64_t d, int32_t dty
   else
     unpool_mean_kernel<float><<<blocks, 256, 0, st>>>(to_dev(L), bh, int(d), dxc, static_cast<float*>(dx));
   VSA_LAUNCH_CHECK("unpool_mean_kernel");
+}
+
+// ============================================================================ tcgen05 (bf16) coarse mode
+// The coarse products on the tensor cores (tcgen05 / TMEM / TMA, the batched GEMM of
+// gemm_sm100.cu) from bf16 copies of the pooled cubes; the fused softmax + top-k +
+// transposed-map kernel is shared with the fp32 mode. The block map may differ from the
+// reference's where bf16 rounding moves a score across the top-k boundary: this mode is
+// validated by feeding the fine stage the oracle's map (north_star), the fp32 mode stays
+// the bit-exact one. Workspace (bf16): qc, kc, vc, dOc [bh, nc, d]; P, dS [bh, nc, nc].
+struct CoarseBf16Ws {
+  __nv_bfloat16 *q, *k, *v, *doc, *p, *ds;
+};
+static CoarseBf16Ws coarse_ws(const vsa_layout_t& L, int64_t bh, int64_t d, void* ws) {
+  auto* b = static_cast<__nv_bfloat16*>(ws);
+  const int64_t cd = bh * L.nc * d, cc = bh * L.nc * L.nc;
+  return {b, b + cd, b + 2 * cd, b + 3 * cd, b + 4 * cd, b + 4 * cd + cc};
+}
+size_t coarse_bf16_ws_bytes(const vsa_layout_t& L, int64_t bh, int64_t d) {
+  return size_t(bh * L.nc * (4 * d + 2 * L.nc)) * 2;
+}
+static int cast3(int64_t n, const float* a, const float* b, const float* c, __nv_bfloat16* x, __nv_bfloat16* y,
+                 __nv_bfloat16* z, cudaStream_t st) {
+  const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  cast_bf16_kernel<<<blocks, 256, 0, st>>>(n, a, b, c, x, y, z);
+  VSA_LAUNCH_CHECK("cast_bf16_kernel");
+}
+
+int launch_coarse_forward_bf16(const vsa_layout_t& L, int64_t bh, int64_t d, const float* qc, const float* kc,
+                               const float* vc, int64_t top_k, float* ac, float* oc_cube, int32_t* sel,
+                               int32_t* selT_offs, int32_t* selT_idx, void* bitmap_ws, void* ws, cudaStream_t st) {
+  const int nc = int(L.nc), D = int(d), B = int(bh);
+  const float scale = 1.0f / std::sqrt(float(d));
+  const CoarseBf16Ws w = coarse_ws(L, bh, d, ws);
+  int rc = cast3(bh * nc * d, qc, kc, vc, w.q, w.k, w.v, st);
+  if (rc) return rc;
+  // scores = (Qc Kc^T) * scale: A = Qc [nc][d] K-major, B = Kc [nc][d] K-major
+  rc = launch_gemm_bf16_batched(false, false, w.q, w.k, B, nc, nc, D, ac, false, scale, st);
+  if (rc) return rc;
+  const bool want_t = selT_offs && selT_idx;
+  uint32_t* bitmap = want_t ? static_cast<uint32_t*>(bitmap_ws) : nullptr;
+  const int words = (nc + 31) / 32;
+  if (bitmap) {
+    rc = cuda_status(cudaMemsetAsync(bitmap, 0, coarse_bitmap_bytes(L, bh), st), "bitmap memset");
+    if (rc) return rc;
+  }
+  {
+    const int64_t rows = bh * nc;
+    const size_t smem = 4 * (nc + 256) * sizeof(uint32_t);
+    rc = cuda_status(
+        cudaFuncSetAttribute(coarse_softmax_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+        "coarse_softmax_topk_kernel: shared memory");
+    if (rc) return rc;
+    coarse_softmax_topk_kernel<<<unsigned((rows + 3) / 4), 128, smem, st>>>(rows, nc, int(top_k), ac, sel, bitmap,
+                                                                            words, w.p);
+    rc = kernel_status("coarse_softmax_topk_kernel");
+    if (rc) return rc;
+  }
+  // Oc = P Vc: A = P [nc][nc] K-major, B = Vc [K = nc][N = d] MN-major
+  rc = launch_gemm_bf16_batched(false, true, w.p, w.v, B, nc, D, nc, oc_cube, false, 1.f, st);
+  if (rc) return rc;
+  if (want_t) return build_csr(L, bh, selT_offs, selT_idx, top_k, bitmap, st);
+  return 0;
+}
+
+int launch_coarse_backward_bf16(const vsa_layout_t& L, int64_t bh, int64_t d, const float* ac,
+                                const float* doc_cube, float* dqc, float* dkc, float* dvc, float* scratch, void* ws,
+                                cudaStream_t st) {
+  const int nc = int(L.nc), D = int(d), B = int(bh);
+  const float scale = 1.0f / std::sqrt(float(d));
+  const CoarseBf16Ws w = coarse_ws(L, bh, d, ws);
+  int rc = cast3(bh * nc * d, doc_cube, nullptr, nullptr, w.doc, nullptr, nullptr, st);
+  if (rc) return rc;
+  // dP = dOc Vc^T: A = dOc [nc][d] K-major, B = Vc [nc][d] K-major
+  rc = launch_gemm_bf16_batched(false, false, w.doc, w.v, B, nc, nc, D, scratch, false, 1.f, st);
+  if (rc) return rc;
+  coarse_bwd_ds_kernel<<<unsigned((bh * nc + 3) / 4), 128, 0, st>>>(bh * nc, nc, scale, ac, scratch, w.ds);
+  rc = kernel_status("coarse_bwd_ds_kernel");
+  if (rc) return rc;
+  // dQc = dS Kc (A K-major, B = Kc [K = nc][N = d] MN-major)
+  rc = launch_gemm_bf16_batched(false, true, w.ds, w.k, B, nc, D, nc, dqc, false, 1.f, st);
+  if (rc) return rc;
+  // dKc = dS^T Qc (A = dS read MN-major), dVc = P^T dOc (A = P read MN-major)
+  rc = launch_gemm_bf16_batched(true, true, w.ds, w.q, B, nc, D, nc, dkc, false, 1.f, st);
+  if (rc) return rc;
+  return launch_gemm_bf16_batched(true, true, w.p, w.doc, B, nc, D, nc, dvc, false, 1.f, st);
 }
 
 }  // namespace vsa_host

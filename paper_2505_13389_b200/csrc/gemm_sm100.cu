@@ -36,7 +36,8 @@ enum { EPI_GATES = 0, EPI_BF16 = 1, EPI_F32 = 2 };
 
 struct GemmEpi {
   int kind;
-  void* c;            // EPI_BF16: bf16 [M][N]; EPI_F32: fp32 [M][N]
+  void* c;            // EPI_BF16: bf16 [batch][M][N]; EPI_F32: fp32 [batch][M][N] (row stride N)
+  float alpha;        // EPI_F32 / EPI_BF16: C = alpha * A.B (1 for the gate products)
   const float* bias;  // EPI_GATES: fp32 [N] or null
   int activation;     // EPI_GATES: VSA_GATE_*
   int adaptation;     // EPI_GATES: Gf == 1
@@ -54,7 +55,7 @@ struct GemmSmall {
 template <bool kAMN, bool kBMN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, int M,
-                           int N, int K, GemmEpi epi) {
+                           int N, int K, int batch, GemmEpi epi) {
   // Persistent over output tiles t = blockIdx.x + i*gridDim.x (tn fastest); the
   // accumulator is double-buffered in TMEM (2 x 256 columns) so the epilogue of tile
   // i overlaps the MMAs of tile i+1, and the TMA ring runs across tile boundaries.
@@ -63,7 +64,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   GemmSmall* sm = reinterpret_cast<GemmSmall*>(smem + kGStages * kGStage);
   const int warp = int(warp_id()), lane = int(lane_id());
   const int nk = (K + kGBK - 1) / kGBK;
-  const int tiles_n = (N + kGBN - 1) / kGBN, tiles = tiles_n * ((M + kGBM - 1) / kGBM);
+  // tiles t = (bi * tiles_m + tm) * tiles_n + tn over the batch (3-D TMA maps: a tile never
+  // reads another batch entry; overhanging rows / cols load as zeros)
+  const int tiles_n = (N + kGBN - 1) / kGBN, tiles_mn = tiles_n * ((M + kGBM - 1) / kGBM);
+  const int tiles = tiles_mn * batch;
 
   if (warp == 1) tmem_alloc<512>(&sm->tmem);
   if (threadIdx.x == 0) {
@@ -88,7 +92,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tma_prefetch_desc(&tm_b);
       int it = 0;  // global k-block counter (ring position)
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t / tiles_n) * kGBM, n0 = (t % tiles_n) * kGBN;
+        const int bi = t / tiles_mn, tmn = t - bi * tiles_mn;
+        const int m0 = (tmn / tiles_n) * kGBM, n0 = (tmn % tiles_n) * kGBN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int st = it % kGStages;
           mbar_wait(&sm->empty[st], ((it / kGStages) & 1) ^ 1);
@@ -99,15 +104,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // K-major: box {64 K, rows}; MN-major: boxes {64 MN, 64 K}, one per 64-wide block
           if (kAMN) {
             for (int blk = 0; blk < kGBM / 64; ++blk)
-              tma_load_2d(a + blk * 8192, &tm_a, &sm->full[st], m0 + blk * 64, k0);
+              tma_load_3d(a + blk * 8192, &tm_a, &sm->full[st], m0 + blk * 64, k0, bi);
           } else {
-            tma_load_2d(a, &tm_a, &sm->full[st], k0, m0);
+            tma_load_3d(a, &tm_a, &sm->full[st], k0, m0, bi);
           }
           if (kBMN) {
             for (int blk = 0; blk < kGBN / 64; ++blk)
-              tma_load_2d(b + blk * 8192, &tm_b, &sm->full[st], n0 + blk * 64, k0);
+              tma_load_3d(b + blk * 8192, &tm_b, &sm->full[st], n0 + blk * 64, k0, bi);
           } else {
-            tma_load_2d(b, &tm_b, &sm->full[st], k0, n0);
+            tma_load_3d(b, &tm_b, &sm->full[st], k0, n0, bi);
           }
         }
       }
@@ -143,8 +148,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int ab = i & 1;
-      const int m0 = (t / tiles_n) * kGBM, n0 = (t % tiles_n) * kGBN;
+      const int bi = t / tiles_mn, tmn = t - bi * tiles_mn;
+      const int m0 = (tmn / tiles_n) * kGBM, n0 = (tmn % tiles_n) * kGBN;
       const int m = m0 + q * 32 + lane;  // this thread's output row
+      const int64_t crow = (int64_t(bi) * M + m) * N;  // EPI_F32 / EPI_BF16 row offset
       const uint32_t lrow = tbase + (uint32_t(q * 32) << 16) + ab * kGBN;
       int gb = 0, gs = 0;  // EPI_GATES: (batch, token) of row m, one division per tile
       if (epi.kind == EPI_GATES) {
@@ -193,20 +200,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int x = 0; x < 8; ++x) w[x] = v[j + x];
             store16(dst + j, w);
           }
-        } else if (epi.kind == EPI_BF16) {
-          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(epi.c) + int64_t(m) * N + n;
+        } else if (epi.kind == EPI_BF16) {  // N % 8 == 0
+          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(epi.c) + crow + n;
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
+            if (n + j >= N) break;
             float w[8];
 #pragma unroll
-            for (int x = 0; x < 8; ++x) w[x] = v[j + x];
+            for (int x = 0; x < 8; ++x) w[x] = v[j + x] * epi.alpha;
             store16(dst + j, w);
           }
         } else {
-          float* dst = static_cast<float*>(epi.c) + int64_t(m) * N + n;
+          float* dst = static_cast<float*>(epi.c) + crow + n;
+          if (n + 32 <= N && (N & 3) == 0) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(dst + j) = make_float4(v[j] * epi.alpha, v[j + 1] * epi.alpha,
+                                                                v[j + 2] * epi.alpha, v[j + 3] * epi.alpha);
+          } else {  // the last, partial column chunk
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n + j < N) dst[j] = v[j] * epi.alpha;
+          }
         }
       }
     }
@@ -277,16 +292,19 @@ namespace vsa_host {
 using namespace vsa_dev;
 
 // Row-major bf16 [rows][cols] map with a box of box_cols (64) x box_rows.
-static bool tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
-  return make_tmap_bf16_sw128(map, base, rows, cols, box_rows);
+static bool tmap_3d(CUtensorMap* map, const void* base, int batch, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  return make_tmap_bf16_sw128_3d(map, base, uint64_t(batch), rows, cols, box_rows);
 }
 
 template <bool kAMN, bool kBMN>
-static int gemm_launch(const void* a, const void* b, int M, int N, int K, const GemmEpi& epi, cudaStream_t st) {
+static int gemm_launch(const void* a, const void* b, int M, int N, int K, const GemmEpi& epi, cudaStream_t st,
+                       int batch = 1) {
   CUtensorMap ta, tb;
-  // A: K-major = [M][K] (box 64 K x 128 rows); MN-major = [K][M] (box 64 M x 64 K rows)
-  const bool ok_a = kAMN ? tmap_2d(&ta, a, uint64_t(K), uint64_t(M), 64) : tmap_2d(&ta, a, uint64_t(M), uint64_t(K), kGBM);
-  const bool ok_b = kBMN ? tmap_2d(&tb, b, uint64_t(K), uint64_t(N), 64) : tmap_2d(&tb, b, uint64_t(N), uint64_t(K), kGBN);
+  // A: K-major = [M][K] (box 64 K x 128 rows); MN-major = [K][M] (box 64 M x 64 K rows); per batch entry
+  const bool ok_a = kAMN ? tmap_3d(&ta, a, batch, uint64_t(K), uint64_t(M), 64)
+                         : tmap_3d(&ta, a, batch, uint64_t(M), uint64_t(K), kGBM);
+  const bool ok_b = kBMN ? tmap_3d(&tb, b, batch, uint64_t(K), uint64_t(N), 64)
+                         : tmap_3d(&tb, b, batch, uint64_t(N), uint64_t(K), kGBN);
   if (!ok_a || !ok_b) {
     set_error("gate GEMM: cuTensorMapEncodeTiled failed");
     return VSA_EINVAL;
@@ -294,12 +312,27 @@ static int gemm_launch(const void* a, const void* b, int M, int N, int K, const 
   const size_t smem = kGStages * kGStage + sizeof(GemmSmall) + 1024;
   auto kern = gemm_bf16_sm100_kernel<kAMN, kBMN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  const int64_t tiles = int64_t((N + kGBN - 1) / kGBN) * ((M + kGBM - 1) / kGBM);
+  const int64_t tiles = int64_t((N + kGBN - 1) / kGBN) * ((M + kGBM - 1) / kGBM) * batch;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  kern<<<unsigned(std::min<int64_t>(tiles, sms)), kGemmThreads, smem, st>>>(ta, tb, M, N, K, epi);
+  kern<<<unsigned(std::min<int64_t>(tiles, sms)), kGemmThreads, smem, st>>>(ta, tb, M, N, K, batch, epi);
   VSA_LAUNCH_CHECK("gemm_bf16_sm100_kernel");
+}
+
+// Batched C[b] = alpha * A[b] . B[b] (bf16 in, fp32 or bf16 out) for the coarse stage's
+// tcgen05 mode: a_mn / b_mn select MN-major operands (A^T / B^T products without copies).
+int launch_gemm_bf16_batched(bool a_mn, bool b_mn, const void* a, const void* b, int batch, int M, int N, int K,
+                             void* c, bool c_bf16, float alpha, cudaStream_t st) {
+  GemmEpi e{};
+  e.kind = c_bf16 ? EPI_BF16 : EPI_F32;
+  e.c = c;
+  e.alpha = alpha;
+  if (!a_mn && !b_mn) return gemm_launch<false, false>(a, b, M, N, K, e, st, batch);
+  if (!a_mn && b_mn) return gemm_launch<false, true>(a, b, M, N, K, e, st, batch);
+  if (a_mn && b_mn) return gemm_launch<true, true>(a, b, M, N, K, e, st, batch);
+  set_error("gemm: A MN-major with B K-major is not instantiated");
+  return VSA_EINVAL;
 }
 
 }  // namespace vsa_host
@@ -365,11 +398,13 @@ extern "C" int vsa_gate_backward(const vsa_layout_t* layout, int64_t batch, int6
   GemmEpi e{};
   e.kind = EPI_BF16;
   e.c = dhidden;
+  e.alpha = 1.f;
   // dhidden[M][md] = dz[M][2Hd] (K-major) . Wg^T: B[n = md][k = 2Hd] = Wg rows (K-major)
   int rc = gemm_launch<false, false>(dz, weight, int(M), int(model_dim), int(N2), e, st);
   if (rc) return rc;
   e.kind = EPI_F32;
   e.c = dweight;
+  e.alpha = 1.f;
   // dWg[md][2Hd] = hidden^T . dz: A[m = md][k = M] = hidden (MN-major), B[n = 2Hd][k = M] = dz (MN-major)
   rc = gemm_launch<true, true>(hidden, dz, int(model_dim), int(N2), int(M), e, st);
   if (rc) return rc;

@@ -56,6 +56,16 @@ int launch_backward_prologue(const vsa_layout_t& L, int64_t bh, int64_t d, int32
                              const void* dout, const void* gc, const void* gf, const float* oc_cube,
                              const void* o_fine, int32_t adaptation, void* dof, float* delta, float* doc_cube,
                              void* dgc, void* dgf, cudaStream_t st);
+// tcgen05 (bf16) coarse mode: batched tensor-core GEMMs + the shared softmax / top-k kernel
+size_t coarse_bf16_ws_bytes(const vsa_layout_t& L, int64_t bh, int64_t d);
+int launch_gemm_bf16_batched(bool a_mn, bool b_mn, const void* a, const void* b, int batch, int M, int N, int K,
+                             void* c, bool c_bf16, float alpha, cudaStream_t st);
+int launch_coarse_forward_bf16(const vsa_layout_t& L, int64_t bh, int64_t d, const float* qc, const float* kc,
+                               const float* vc, int64_t top_k, float* ac, float* oc_cube, int32_t* sel,
+                               int32_t* selT_offs, int32_t* selT_idx, void* bitmap_ws, void* ws, cudaStream_t st);
+int launch_coarse_backward_bf16(const vsa_layout_t& L, int64_t bh, int64_t d, const float* ac,
+                                const float* doc_cube, float* dqc, float* dkc, float* dvc, float* scratch, void* ws,
+                                cudaStream_t st);
 int launch_coarse_backward(const vsa_layout_t& L, int64_t bh, int64_t d, const float* qc, const float* kc,
                            const float* vc, const float* ac, const float* doc_cube, float* dqc, float* dkc,
                            float* dvc, float* scratch, cudaStream_t st);

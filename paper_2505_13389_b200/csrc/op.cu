@@ -31,7 +31,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Plan {
   size_t q_t, k_t, v_t, qc, kc, vc, ac, oc, sel, selT_offs, selT_idx, bitmap, o_f, lse, dof, delta, doc, dqc, dkc,
-      dvc, scratch, gc, gf, dgc, dgf, dz, valid_err, total;
+      dvc, scratch, gc, gf, dgc, dgf, dz, valid_err, coarse_ws, total;
 };
 
 Plan make_plan(const vsa_layout_t& L, const vsa_op_desc_t& D) {
@@ -73,6 +73,7 @@ Plan make_plan(const vsa_layout_t& L, const vsa_op_desc_t& D) {
   take(p.dgc, gates ? bh * S_io * d * es : 0);
   take(p.dgf, gates ? bh * S_io * d * es : 0);
   take(p.valid_err, 16);
+  take(p.coarse_ws, vsa_coarse_workspace_bytes(&L, int64_t(bh), int64_t(d), D.coarse));
   p.dz = 0;
   p.total = off;
   return p;
@@ -130,6 +131,9 @@ int check_desc(const vsa_layout_t* L, const vsa_op_desc_t* D) {
   VSA_REQUIRE(D->activation == VSA_GATE_IDENTITY || D->activation == VSA_GATE_SIGMOID,
               "VsaParams: unknown gate activation");
   VSA_REQUIRE(D->model_dim >= 0, "VsaParams: model_dim must be >= 0");
+  VSA_REQUIRE(D->coarse == VSA_COARSE_F32 || D->coarse == VSA_COARSE_BF16, "vsa_op: unknown coarse precision");
+  if (D->coarse == VSA_COARSE_BF16)
+    VSA_REQUIRE(L->nc % 8 == 0 && D->head_dim % 8 == 0, "vsa_op: the bf16 coarse mode needs nc % 8 == 0");
   if (L->io_order == VSA_IO_SEQ_MAJOR) {
     VSA_REQUIRE(D->raster, "sequence-major I/O needs raster order");
     VSA_REQUIRE(L->io_batch == D->batch && L->io_heads == D->heads, "sequence-major I/O: layout batch/heads mismatch");
@@ -300,10 +304,11 @@ int vsa_op_forward_coarse(vsa_op_t* op, const void* q, const void* k, const void
     if (rc) return rc;
     VSA_REQUIRE(herr == 0, "BlockSelection: indices must be strictly ascending and in [0, num_cubes)");
   }
-  rc = vsa_coarse_forward(L, bh, d, pooled[0], pooled[1], pooled[2], D.top_k, op->at<float>(p.ac),
-                          op->at<float>(p.oc), op->at<int32_t>(p.sel),
-                          override_sel ? nullptr : op->at<int32_t>(p.selT_offs),
-                          override_sel ? nullptr : op->at<int32_t>(p.selT_idx), op->at(p.bitmap), stream);
+  rc = vsa_coarse_forward_ex(L, bh, d, pooled[0], pooled[1], pooled[2], D.top_k, D.coarse, op->at<float>(p.ac),
+                             op->at<float>(p.oc), op->at<int32_t>(p.sel),
+                             override_sel ? nullptr : op->at<int32_t>(p.selT_offs),
+                             override_sel ? nullptr : op->at<int32_t>(p.selT_idx), op->at(p.bitmap),
+                             op->at(p.coarse_ws), stream);
   if (rc) return rc;
   if (override_sel) {
     rc = vsa_selection_transpose(L, bh, sel_override, sel_k, op->at<int32_t>(p.selT_offs),
@@ -371,9 +376,9 @@ int vsa_op_backward(vsa_op_t* op, const void* dout, void* dq, void* dk, void* dv
     if (rc) return rc;
   }
   record(op, op->ev_b, call, 1, st);
-  rc = vsa_coarse_backward(L, bh, d, op->at<float>(p.qc), op->at<float>(p.kc), op->at<float>(p.vc),
-                           op->at<float>(p.ac), op->at<float>(p.doc), op->at<float>(p.dqc), op->at<float>(p.dkc),
-                           op->at<float>(p.dvc), op->at<float>(p.scratch), stream);
+  rc = vsa_coarse_backward_ex(L, bh, d, op->at<float>(p.qc), op->at<float>(p.kc), op->at<float>(p.vc),
+                              op->at<float>(p.ac), op->at<float>(p.doc), op->at<float>(p.dqc), op->at<float>(p.dkc),
+                              op->at<float>(p.dvc), op->at<float>(p.scratch), D.coarse, op->at(p.coarse_ws), stream);
   if (rc) return rc;
   record(op, op->ev_b, call, 2, st);
   const bool mean = D.pool_mode == VSA_POOL_MEAN;

@@ -41,4 +41,21 @@ inline bool make_tmap_bf16_sw128(CUtensorMap* map, const void* base, uint64_t ro
   return r == CUDA_SUCCESS;
 }
 
+// Batched row-major bf16 tensor [batch][rows][cols] (cols contiguous), box = 64 cols x
+// box_rows x 1, SWIZZLE_128B; out-of-bounds rows / cols of a box read as zeros (so tiles
+// may overhang a matrix of any size without touching the next batch entry).
+inline bool make_tmap_bf16_sw128_3d(CUtensorMap* map, const void* base, uint64_t batch, uint64_t rows, uint64_t cols,
+                                    uint32_t box_rows) {
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn || (cols * 2) % 16 != 0) return false;
+  cuuint64_t dims[3] = {cols, rows, batch};
+  cuuint64_t strides[2] = {cols * 2, rows * cols * 2};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace vsa_host
