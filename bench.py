@@ -182,17 +182,30 @@ def run_ours(args, rank, world, local_rank):
 
     # batch x head partition of the ONE problem: this rank's contiguous unit
     # range, no data-path collective (strong scaling; paper_2505_13389_b200/partition.py)
-    from paper_2505_13389_b200.partition import partition_units
+    from paper_2505_13389_b200.partition import SubSplitVsa, partition_tasks, partition_units
 
     units = cfg["B"] * cfg["H"]
-    parts = partition_units(units, world)
-    u0, u1 = parts[rank]
+    # whole units per rank when they divide evenly; otherwise the (unit, cube) task sub-split
+    # (heads shared between ranks, lse / delta exchanged with one all-reduce each)
+    split = world > 1 and units % world != 0
+    if split:
+        part = SubSplitVsa(L, cfg["B"], cfg["H"], d, K, rank, world, coarse=args.coarse)
+        op, u0, u1 = part.op, part.ua, part.ub
+        parts = partition_tasks(units, nc, world)
+    else:
+        part = None
+        parts = partition_units(units, world)
+        u0, u1 = parts[rank]
+        op = vsa.VsaOp(L, 1, u1 - u0, d, K, dtype=dtype, coarse=args.coarse) if u1 > u0 else None
     n = u1 - u0
-    op = vsa.VsaOp(L, 1, n, d, K, dtype=dtype, coarse=args.coarse) if n else None
     q, k, v, gc, gf, do = make_inputs(cfg, S, dtype, dev, u0, u1)
     outs = [torch.empty_like(q) for _ in range(6)]
 
     def step():
+        if split:
+            part.forward(q, k, v, gc, gf, out=outs[0], check_inputs=False)
+            part.backward(do, *outs[1:], check_inputs=False)
+            return
         if op is None:
             return
         op.forward(q, k, v, gc, gf, out=outs[0], check_inputs=False)
@@ -238,7 +251,7 @@ def run_ours(args, rank, world, local_rank):
 
     # the other coarse mode (fp32 canonical <-> bf16 tcgen05), same inputs: step and coarse times
     other_coarse = None
-    if op is not None and world == 1 and L.num_cubes % 8 == 0:
+    if op is not None and world == 1 and L.num_cubes % 8 == 0 and not split:
         alt = "bf16" if args.coarse == "fp32" else "fp32"
         opa = vsa.VsaOp(L, 1, n, d, K, dtype=dtype, coarse=alt)
 
@@ -266,7 +279,7 @@ def run_ours(args, rank, world, local_rank):
 
     # dense baseline: the same kernels with top-k = all cubes
     dense = None
-    if not args.no_dense:
+    if not args.no_dense and not split:
         opd = vsa.VsaOp(L, 1, n, d, nc, dtype=dtype) if n else None
         fld = flops(cfg, nc, nc, d)
 
@@ -323,13 +336,24 @@ def run_ours(args, rank, world, local_rank):
     # H2D of unit-group i+1 and the D2H of group i-1 with the kernels of group i
     hin = [t.cpu().pin_memory() for t in (q, k, v, gc, gf, do)]
     hout = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
-    del op  # free the resident-input operator's buffers before building the pipeline
-    torch.cuda.empty_cache()
-    pipe = vsa.VsaHostPipeline(L, 1, n, d, K, chunks=min(args.e2e_chunks, n), dtype=dtype) if n else None
+    if not split:
+        del op  # free the resident-input operator's buffers before building the pipeline
+        torch.cuda.empty_cache()
+    pipe = (vsa.VsaHostPipeline(L, 1, n, d, K, chunks=min(args.e2e_chunks, n), dtype=dtype) if n and not split
+            else None)
+    if split:  # the sub-split op stays; its inputs come from host every step
+        op = part.op
+        q, k, v, gc, gf, do = (torch.empty_like(t) for t in (q, k, v, gc, gf, do))
 
     def e2e_step():
         if pipe is not None:
             pipe.run(hin, hout)
+        elif split:
+            for dst, src in zip((q, k, v, gc, gf, do), hin):
+                dst.copy_(src, non_blocking=True)
+            step()
+            for dst, src in zip(hout, outs):
+                dst.copy_(src, non_blocking=True)
 
     e2e_step()
     barrier()
@@ -353,7 +377,8 @@ def run_ours(args, rank, world, local_rank):
         return None
 
     # roofline of the dominant kernel (rank 0's share of the work: n units)
-    fl_r = flops(dict(B=1, H=max(n, 1)), nc, K, d)
+    n_eff = (part.t1 - part.t0) / nc if split else n  # units' worth of rank 0's tasks
+    fl_r = flops(dict(B=1, H=max(n_eff, 1e-9)), nc, K, d)
     dom = max(("fine_fwd", "fine_bwd"), key=lambda s: stage_ms[s])
     ach = fl_r[dom] / (max(stage_ms[dom], 1e-9) * 1e-3) / 1e12
     traffic = None
@@ -378,7 +403,7 @@ def run_ours(args, rank, world, local_rank):
                          for k in ks if k.get("smem_tc_wavefronts_pct")}
         except Exception:
             smem_pipe = None
-    bytes_tp = n * 3 * (S * d * 2 + L.seq_padded * d * 2 + nc * d * 4)
+    bytes_tp = n * 3 * (S * d * 2 + L.seq_padded * d * 2 + nc * d * 4)  # K1 runs on whole units
     stages = {}
     for s in STAGES:
         e = {"ms": round(stage_ms[s], 4)}
@@ -404,9 +429,11 @@ def run_ours(args, rank, world, local_rank):
             "workload": cfg["workload"], "B": cfg["B"], "H": cfg["H"], "head_dim": d, "grid": list(cfg["grid"]),
             "grid_padded": list(L.padded), "cube": [4, 4, 4], "num_cubes": nc, "top_k": K,
             "sparsity": round(1 - K / nc, 4), "global_batch": cfg["B"], "seq_len": S,
-            "parallelism": f"bh{world}: batch x head partition of one problem, "
-                           f"{min(b - a for a, b in parts)}-{max(b - a for a, b in parts)} of {units} (b,h) units "
-                           f"per GPU, no collective",
+            "parallelism": (f"bh{world}: batch x head partition of one problem, "
+                            f"{min(b - a for a, b in parts)}-{max(b - a for a, b in parts)} of {units} (b,h) units "
+                            f"per GPU, no collective") if not split else
+                           (f"bh{world}+cube split: {min(b - a for a, b in parts)}-{max(b - a for a, b in parts)} of "
+                            f"{units * nc} (unit, cube) tasks per GPU, lse / delta all-reduce of shared heads"),
             "l2": "inputs larger than L2 (6 x {:.0f} MB bf16 per step)".format(q.numel() * 2 / 1e6),
             "flops_per_step": fl["total"],
         },

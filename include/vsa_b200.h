@@ -180,6 +180,23 @@ int vsa_fine_forward(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t 
                      const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse, float* row_max,
                      const void* gc, const void* gf, const float* oc_cube, int32_t flags, void* out, void* stream);
 
+/* Task-range variants (a head sub-split across GPUs): the forward computes
+ * only query cubes t = u*nc + qc in [task_begin, task_end) (their out / o_fine / lse rows);
+ * the backward computes dQ for those query cubes and dK/dV for the key cubes of the same
+ * range. lse and delta must hold every query row of the units involved (a rank exchanges
+ * its rows with the ranks sharing a unit); dQ then recomputes S / dP (no dS workspace: the
+ * dS tiles of a query cube come from other ranks' key cubes). tcgen05 path only. */
+int vsa_fine_forward_range(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* q,
+                           const void* k, const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse,
+                           float* row_max, const void* gc, const void* gf, const float* oc_cube, int32_t flags,
+                           void* out, int64_t task_begin, int64_t task_end, void* stream);
+int vsa_fine_backward_range(const vsa_layout_t* layout, int64_t bh, int64_t d, int32_t dtype, const void* q,
+                            const void* k, const void* v, const void* dof, const float* lse, const float* delta,
+                            const int32_t* sel, int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx,
+                            const float* dqc, const float* dkc, const float* dvc, int32_t raster, int32_t flags,
+                            void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes, int64_t task_begin,
+                            int64_t task_end, void* stream);
+
 /* K6a — backward prologue, the elementwise part of vsa_backward (vsa.hpp:142-150)
  * fused with the tile of dO and the fine delta:
  *   dof  = dO*Gf (tiled, dtype)                 dgc = dO*Oc  (same order as dout)
@@ -286,6 +303,12 @@ typedef struct vsa_op_desc_t {
   int32_t raster;      /* 1: q/k/v/gates/out/dO/grads raster-ordered (tiling fused); 0: tile-ordered (vsa.hpp:86) */
   int32_t flags;       /* VSA_OP_* */
   int32_t coarse;      /* VSA_COARSE_F32 (bit-exact map, default) or VSA_COARSE_BF16 (tcgen05) */
+  int32_t reserved;
+  /* Sub-split: the fine stages compute only the (unit, cube) tasks
+   * t = u*nc + c in [task_begin, task_end) of this op's units (0, 0 = all). Between
+   * vsa_op_forward and vsa_op_backward_finish the caller completes lse (after the forward)
+   * and delta (after vsa_op_backward_prologue) with the rows of the other ranks. */
+  int64_t task_begin, task_end;
 } vsa_op_desc_t;
 
 /* Device pointers of the context's buffers (views for callers and tests). */
@@ -326,9 +349,13 @@ int vsa_op_forward(vsa_op_t* op, const void* q, const void* k, const void* v, co
 int vsa_op_forward_coarse(vsa_op_t* op, const void* q, const void* k, const void* v, const int32_t* sel_override,
                           int64_t sel_k, void* stream);
 int vsa_op_forward_fine(vsa_op_t* op, const void* gc, const void* gf, void* out, void* stream);
-/* Attention-level backward: dO -> dq, dk, dv, dgc, dgf (dgc/dgf may be NULL). */
+/* Attention-level backward: dO -> dq, dk, dv, dgc, dgf (dgc/dgf may be NULL) =
+ * vsa_op_backward_prologue (K6a + K6d: dof, delta, dgc, dgf, coarse cube gradients) then
+ * vsa_op_backward_finish (K6b/K6c + unpool). */
 int vsa_op_backward(vsa_op_t* op, const void* dout, void* dq, void* dk, void* dv, void* dgc, void* dgf,
                     void* stream);
+int vsa_op_backward_prologue(vsa_op_t* op, const void* dout, void* dgc, void* dgf, void* stream);
+int vsa_op_backward_finish(vsa_op_t* op, void* dq, void* dk, void* dv, void* stream);
 
 /* Replaces: vsa_forward (vsa.hpp:89-122). hidden: bf16 [B, S, model_dim] in the op's row
  * order (raster tokens, or tile order when desc.raster == 0); gate_weight bf16

@@ -31,7 +31,8 @@ class vsa_layout_t(C.Structure):
 
 class vsa_op_desc_t(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("batch", "heads", "head_dim", "top_k", "max_sel_k", "model_dim")] + [
-        (n, C.c_int32) for n in ("dtype", "pool_mode", "activation", "adaptation", "raster", "flags", "coarse")]
+        (n, C.c_int32) for n in ("dtype", "pool_mode", "activation", "adaptation", "raster", "flags", "coarse",
+                                 "reserved")] + [("task_begin", C.c_int64), ("task_end", C.c_int64)]
 
 
 class vsa_op_buffers_t(C.Structure):
@@ -56,7 +57,8 @@ EXPORTS = [
     "vsa_op_memory_bytes", "vsa_op_create", "vsa_op_destroy", "vsa_op_buffers", "vsa_op_set_workspace",
     "vsa_op_workspace_bytes", "vsa_op_forward", "vsa_op_forward_coarse", "vsa_op_forward_fine", "vsa_op_backward",
     "vsa_forward", "vsa_backward", "vsa_op_timing", "vsa_op_stage_ms", "vsa_coarse_backward_tokens",
-    "vsa_coarse_workspace_bytes", "vsa_coarse_forward_ex", "vsa_coarse_backward_ex",
+    "vsa_coarse_workspace_bytes", "vsa_coarse_forward_ex", "vsa_coarse_backward_ex", "vsa_fine_forward_range",
+    "vsa_fine_backward_range", "vsa_op_backward_prologue", "vsa_op_backward_finish",
 ]
 
 
@@ -122,6 +124,11 @@ def lib():
         "vsa_op_forward_coarse": [P, P, P, P, P, I64, P],
         "vsa_op_forward_fine": [P, P, P, P, P],
         "vsa_op_backward": [P, P, P, P, P, P, P, P],
+        "vsa_op_backward_prologue": [P, P, P, P, P],
+        "vsa_op_backward_finish": [P, P, P, P, P],
+        "vsa_fine_forward_range": [LP, I64, I64, I32, P, P, P, P, I64, P, P, P, P, P, P, I32, P, I64, I64, P],
+        "vsa_fine_backward_range": [LP, I64, I64, I32, P, P, P, P, P, P, P, I64, P, P, P, P, P, I32, I32, P, P, P, P,
+                                    C.c_size_t, I64, I64, P],
         "vsa_forward": [P, P, P, P, P, P, P, P, I64, P, P],
         "vsa_backward": [P, P, P, P, P, P, P, P, P, P, P],
         "vsa_op_timing": [P, I32],

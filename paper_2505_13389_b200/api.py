@@ -377,10 +377,13 @@ class VsaOp:
     def __init__(self, layout: TileLayout, B: int, H: int, d: int, top_k: int, dtype=torch.bfloat16,
                  pool: int = POOL_MEAN, adaptation: bool = False, raster: bool = True, device="cuda",
                  force_simt: bool = False, bwd_workspace: bool = True, io: str = "bhsd", seq_chunks: int = 1,
-                 max_sel_k: int = 0, model_dim: int = 0, activation: int = GATE_IDENTITY, coarse: str = "fp32"):
+                 max_sel_k: int = 0, model_dim: int = 0, activation: int = GATE_IDENTITY, coarse: str = "fp32",
+                 task_range=None):
         if coarse not in ("fp32", "bf16"):
             raise ValueError("coarse must be 'fp32' (bit-exact block map) or 'bf16' (tcgen05)")
         self.coarse = coarse
+        # sub-split: the fine stages compute only (unit, cube) tasks [t0, t1)
+        self.task_range = (0, 0) if task_range is None else (int(task_range[0]), int(task_range[1]))
         if not (1 <= top_k <= layout.num_cubes):
             raise ValueError("coarse_forward_select: k must be in [1, num_cubes]")
         if io not in ("bhsd", "bshd"):
@@ -422,7 +425,7 @@ class VsaOp:
         desc = L.vsa_op_desc_t(self.B, self.H, self.d, self.top_k, max_sel_k, self.model_dim,
                                L.VSA_BF16 if self.dtype == torch.bfloat16 else L.VSA_F32, int(self.pool),
                                self.activation, 1 if self.adaptation else 0, 1 if self.raster else 0, flags,
-                               L.COARSE_BF16 if self.coarse == "bf16" else L.COARSE_F32)
+                               L.COARSE_BF16 if self.coarse == "bf16" else L.COARSE_F32, 0, *self.task_range)
         nbytes = lib.vsa_op_memory_bytes(self._lref, C.byref(desc))
         h = C.c_void_p()
         if nbytes == 0:  # invalid descriptor: let create report the reference's message
@@ -570,8 +573,11 @@ class VsaOp:
         """Whether the last backward took the dS-materialising path (else dQ recomputed S / dP)."""
         return bool(self._bufs().bwd_used_workspace)
 
-    def backward(self, dout, dq=None, dk=None, dv=None, dgc=None, dgf=None, check_inputs=True):
-        """vsa_backward (vsa.hpp:129-189) at attention level -> (dq, dk, dv, dgc, dgf)."""
+    def backward(self, dout, dq=None, dk=None, dv=None, dgc=None, dgf=None, check_inputs=True, before_finish=None):
+        """vsa_backward (vsa.hpp:129-189) at attention level -> (dq, dk, dv, dgc, dgf).
+
+        ``before_finish``: optional callable run between the prologue (dof, delta, gate and
+        coarse gradients) and the fine backward."""
         if getattr(self, "_fwd", None) is None:
             raise ValueError("vsa_backward: missing or mismatched forward artifacts")
         if check_inputs:
@@ -583,7 +589,11 @@ class VsaOp:
         dgc = mk() if dgc is None else dgc
         dgf = mk() if dgf is None else dgf
         self._ensure_workspace(dout.device)
-        check(self._lib.vsa_op_backward(self._h, _p(dout), _p(dq), _p(dk), _p(dv), _p(dgc), _p(dgf), _stream()))
+        st = _stream()
+        check(self._lib.vsa_op_backward_prologue(self._h, _p(dout), _p(dgc), _p(dgf), st))
+        if before_finish is not None:  # e.g. complete delta with the other ranks' rows (sub-split)
+            before_finish()
+        check(self._lib.vsa_op_backward_finish(self._h, _p(dq), _p(dk), _p(dv), st))
         return dq, dk, dv, dgc, dgf
 
     # -- the reference's vsa_forward / vsa_backward with hidden states (model_dim > 0)

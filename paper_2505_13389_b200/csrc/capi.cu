@@ -274,15 +274,18 @@ int vsa_validate_selection(const int32_t* sel, int64_t rows, int64_t top_k, int6
   return launch_validate_selection(sel, rows, top_k, nc, err_dev, as_stream(stream));
 }
 
-int vsa_fine_forward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* q, const void* k,
-                     const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse, float* row_max,
-                     const void* gc, const void* gf, const float* oc_cube, int32_t flags, void* out, void* stream) {
+int vsa_fine_forward_range(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* q, const void* k,
+                           const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse, float* row_max,
+                           const void* gc, const void* gf, const float* oc_cube, int32_t flags, void* out,
+                           int64_t task_begin, int64_t task_end, void* stream) {
   VSA_CHECKED(check_layout(L));
   VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(dtype_ok(dtype), "fine stage: unknown dtype");
   VSA_REQUIRE(q && k && v && sel && o_fine && lse && bh >= 1, "fine stage: null buffer");
   VSA_REQUIRE(top_k >= 1 && top_k <= L->nc, "fine stage: selection does not match shapes");
   VSA_REQUIRE(d >= 1 && L->cube <= 128 && L->cube * d <= 8192, "fine stage: cube*head_dim > 8192 unsupported");
+  VSA_REQUIRE(task_begin >= 0 && task_begin < task_end && task_end <= bh * L->nc,
+              "fine stage: task range must be a non-empty part of [0, bh*nc)");
   if (flags & VSA_FINE_COMBINE)
     VSA_REQUIRE(out && gc && oc_cube && (gf || (flags & VSA_FINE_ADAPTATION)), "combine: missing gates / Oc");
   if (flags & VSA_FINE_UNTILE) VSA_REQUIRE(out != nullptr, "untile: missing output");
@@ -294,9 +297,18 @@ int vsa_fine_forward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype
                 "fine stage: bf16 needs 64-token cubes and head_dim 64 or 128 (VSA_FINE_FORCE_SIMT for the SIMT path)");
   if (!(flags & VSA_FINE_FORCE_SIMT) && sm100_fine_supported(*L, d, dtype))
     return launch_fine_forward_sm100(*L, bh, d, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube, flags,
-                                     out, st);
+                                     out, task_begin, task_end, st);
+  VSA_REQUIRE(task_begin == 0 && task_end == bh * L->nc, "fine stage: task ranges need the tcgen05 kernels");
   return launch_fine_forward_simt(*L, bh, d, dtype, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube,
                                   flags, out, st);
+}
+
+int vsa_fine_forward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* q, const void* k,
+                     const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse, float* row_max,
+                     const void* gc, const void* gf, const float* oc_cube, int32_t flags, void* out, void* stream) {
+  VSA_CHECKED(check_layout(L));
+  return vsa_fine_forward_range(L, bh, d, dtype, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube, flags,
+                                out, 0, bh * L->nc, stream);
 }
 
 int vsa_backward_prologue(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, int32_t raster,
@@ -325,11 +337,12 @@ int vsa_coarse_backward(const vsa_layout_t* L, int64_t bh, int64_t d, const floa
   return launch_coarse_backward(*L, bh, d, qc, kc, vc, ac, doc_cube, dqc, dkc, dvc, scratch, as_stream(stream));
 }
 
-int vsa_fine_backward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* q, const void* k,
-                      const void* v, const void* dof, const float* lse, const float* delta, const int32_t* sel,
-                      int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx, const float* dqc,
-                      const float* dkc, const float* dvc, int32_t raster, int32_t flags, void* dq, void* dk,
-                      void* dv, void* workspace, size_t workspace_bytes, void* stream) {
+int vsa_fine_backward_range(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* q, const void* k,
+                            const void* v, const void* dof, const float* lse, const float* delta, const int32_t* sel,
+                            int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx, const float* dqc,
+                            const float* dkc, const float* dvc, int32_t raster, int32_t flags, void* dq, void* dk,
+                            void* dv, void* workspace, size_t workspace_bytes, int64_t task_begin, int64_t task_end,
+                            void* stream) {
   VSA_CHECKED(check_layout(L));
   VSA_CHECKED(check_io(L, bh));
   VSA_REQUIRE(dtype_ok(dtype), "fine_backward: unknown dtype");
@@ -338,15 +351,28 @@ int vsa_fine_backward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtyp
   VSA_REQUIRE(selT_offs && selT_idx, "fine_backward: transposed block map required");
   VSA_REQUIRE(top_k >= 1 && top_k <= L->nc, "fine stage: selection does not match shapes");
   VSA_REQUIRE(d >= 1 && L->cube <= 128 && L->cube * d <= 8192, "fine stage: cube*head_dim > 8192 unsupported");
+  VSA_REQUIRE(task_begin >= 0 && task_begin < task_end && task_end <= bh * L->nc,
+              "fine_backward: task range must be a non-empty part of [0, bh*nc)");
   cudaStream_t st = as_stream(stream);
   if (dtype == VSA_BF16 && !(flags & VSA_FINE_FORCE_SIMT))
     VSA_REQUIRE(sm100_fine_bwd_supported(*L, d, dtype),
                 "fine_backward: bf16 needs 64-token cubes and head_dim 64 or 128 (VSA_FINE_FORCE_SIMT for the SIMT path)");
   if (!(flags & VSA_FINE_FORCE_SIMT) && sm100_fine_bwd_supported(*L, d, dtype))
     return launch_fine_backward_sm100(*L, bh, d, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc,
-                                      dvc, raster, dq, dk, dv, workspace, workspace_bytes, st);
+                                      dvc, raster, dq, dk, dv, workspace, workspace_bytes, task_begin, task_end, st);
+  VSA_REQUIRE(task_begin == 0 && task_end == bh * L->nc, "fine_backward: task ranges need the tcgen05 kernels");
   return launch_fine_backward_simt(*L, bh, d, dtype, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc,
                                    dkc, dvc, raster, dq, dk, dv, st);
+}
+
+int vsa_fine_backward(const vsa_layout_t* L, int64_t bh, int64_t d, int32_t dtype, const void* q, const void* k,
+                      const void* v, const void* dof, const float* lse, const float* delta, const int32_t* sel,
+                      int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx, const float* dqc,
+                      const float* dkc, const float* dvc, int32_t raster, int32_t flags, void* dq, void* dk,
+                      void* dv, void* workspace, size_t workspace_bytes, void* stream) {
+  VSA_CHECKED(check_layout(L));
+  return vsa_fine_backward_range(L, bh, d, dtype, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc,
+                                 dvc, raster, flags, dq, dk, dv, workspace, workspace_bytes, 0, bh * L->nc, stream);
 }
 
 size_t vsa_fine_backward_workspace_bytes(const vsa_layout_t* L, int64_t bh, int64_t top_k) {

@@ -203,7 +203,7 @@ template <int D>
 __global__ void __launch_bounds__(kKVThreads, 1)
     fine_dkdv_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                           DevLayout L, int ntasks, int k_sel, float scale, float scale_log2,
+                           DevLayout L, int task0, int ntasks, int k_sel, float scale, float scale_log2,
                            const float* __restrict__ lse, const float* __restrict__ delta,
                            const int32_t* __restrict__ offs, const int32_t* __restrict__ idx,
                            const float* __restrict__ dkc, const float* __restrict__ dvc, int raster,
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         mbar_wait(&sm->task_empty[slot], ((j / kTaskRing) & 1) ^ 1);
         // without a workspace (no counter): static round-robin hand-out
         int t = task_ctr ? atomicAdd(task_ctr, 1) : int(blockIdx.x) + j * int(gridDim.x);
-        if (t >= ntasks) t = -1;
+        t = (t >= ntasks) ? -1 : task0 + t;  // (unit, key cube) tasks [task0, task0 + ntasks)
         sm->task_id[slot] = t;
         mbar_arrive(&sm->task_full[slot]);
         if (t < 0) break;
@@ -705,7 +705,7 @@ struct DQSmall {
 template <int D>
 __global__ void __launch_bounds__(kDQThreads, 2)
     fine_dq_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_ds,
-                              DevLayout L, int k_sel, float scale, const int32_t* __restrict__ sel,
+                              DevLayout L, int task0, int k_sel, float scale, const int32_t* __restrict__ sel,
                               const float* __restrict__ dqc, int raster, __nv_bfloat16* __restrict__ dq) {
   using C = DQCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -713,8 +713,9 @@ __global__ void __launch_bounds__(kDQThreads, 2)
   uint8_t* sZ = smem + C::kOffZ;
   DQSmall* sm = reinterpret_cast<DQSmall*>(smem + C::kTiles);
   const int warp = int(warp_id()), lane = int(lane_id());
-  const int qc = blockIdx.x;
-  const int64_t u = blockIdx.y;
+  const int64_t task = int64_t(task0) + blockIdx.x;  // one CTA per (unit, query cube)
+  const int64_t u = task / L.nc;
+  const int qc = int(task - u * L.nc);
   const int npairs = (k_sel + 1) >> 1;
   const int32_t* srow = sel + (u * L.nc + qc) * int64_t(k_sel);
   const int row0 = int(u * L.seqp);
@@ -871,9 +872,10 @@ template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     fine_dq_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                         DevLayout L, int k_sel, float scale, float scale_log2, const float* __restrict__ lse,
-                         const float* __restrict__ delta, const int32_t* __restrict__ sel,
-                         const float* __restrict__ dqc, int raster, __nv_bfloat16* __restrict__ dq) {
+                         DevLayout L, int task0, int k_sel, float scale, float scale_log2,
+                         const float* __restrict__ lse, const float* __restrict__ delta,
+                         const int32_t* __restrict__ sel, const float* __restrict__ dqc, int raster,
+                         __nv_bfloat16* __restrict__ dq) {
   using C = QCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
@@ -886,8 +888,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   QSmall* sm = reinterpret_cast<QSmall*>(smem + C::kTiles);
 
   const int warp = int(warp_id()), lane = int(lane_id());
-  const int qc = blockIdx.x;
-  const int64_t u = blockIdx.y;
+  const int64_t task = int64_t(task0) + blockIdx.x;  // one CTA per (unit, query cube)
+  const int64_t u = task / L.nc;
+  const int qc = int(task - u * L.nc);
   const int npairs = (k_sel + 1) >> 1;
   const int32_t* srow = sel + (u * L.nc + qc) * int64_t(k_sel);
   const int row0 = int(u * L.seqp);
@@ -1091,7 +1094,8 @@ template <int D>
 static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const void* k, const void* v,
                       const void* dof, const float* lse, const float* delta, const int32_t* sel, int64_t top_k,
                       const int32_t* offs, const int32_t* idx, const float* dqc, const float* dkc, const float* dvc,
-                      int32_t raster, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, cudaStream_t st) {
+                      int32_t raster, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t task_begin,
+                      int64_t task_end, cudaStream_t st) {
   CUtensorMap tq, tk, tv, tdo, tds;
   const uint64_t rows = uint64_t(bh * Lh.seq_padded);
   if (!make_tmap_bf16_sw128(&tq, q, rows, D, 64) || !make_tmap_bf16_sw128(&tk, k, rows, D, 64) ||
@@ -1101,7 +1105,11 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
   }
   // dS materialisation needs the workspace (bf16 tiles + CSR positions); without it
   // dQ recomputes S and dP (the fallback kernel).
-  const bool store_ds = ws != nullptr && ws_bytes >= fine_backward_ws_bytes(Lh, bh, top_k);
+  // a partial task range (a rank's share of sub-split heads) cannot use stored dS: the dS
+  // tiles of its query cubes come from the key cubes of the other ranks
+  const bool full = task_begin == 0 && task_end == bh * Lh.nc;
+  const bool store_ds = full && ws != nullptr && ws_bytes >= fine_backward_ws_bytes(Lh, bh, top_k);
+  const int64_t ntask = task_end - task_begin;
   const int64_t tiles = bh * Lh.nc * top_k;
   int32_t* pos = store_ds ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + tiles * 8192) : nullptr;
   if (store_ds && !make_tmap_bf16_sw128(&tds, ws, uint64_t(tiles) * 64, 64, 64)) {
@@ -1112,7 +1120,7 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
   const float scale = 1.0f / std::sqrt(float(D));
   const float scale_log2 = scale * 1.4426950408889634f;
   const DevLayout L = to_dev(Lh);
-  dim3 grid(unsigned(Lh.nc), unsigned(bh));
+  const unsigned grid = unsigned(ntask);  // dQ: one CTA per (unit, query cube) of the range
   if (store_ds) {
     const int blocks = int(std::min<int64_t>((tiles + 255) / 256, 148 * 8));
     selT_positions_kernel<<<blocks, 256, 0, st>>>(bh, int(Lh.nc), int(top_k), sel, offs, idx, pos);
@@ -1122,8 +1130,8 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
     const size_t smem = QCfg<D>::kTiles + sizeof(QSmall) + 1024;
     auto kern = fine_dq_sm100_kernel<D>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    kern<<<grid, kBwdThreads, smem, st>>>(tq, tk, tv, tdo, L, int(top_k), scale, scale_log2, lse, delta, sel, dqc,
-                                         raster, static_cast<__nv_bfloat16*>(dq));
+    kern<<<grid, kBwdThreads, smem, st>>>(tq, tk, tv, tdo, L, int(task_begin), int(top_k), scale, scale_log2, lse,
+                                         delta, sel, dqc, raster, static_cast<__nv_bfloat16*>(dq));
     int rc = kernel_status("fine_dq_sm100_kernel");
     if (rc) return rc;
   }
@@ -1134,12 +1142,12 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t ntasks = bh * Lh.nc;  // persistent: one CTA per SM over the (unit, key cube) tasks
+    const int64_t ntasks = ntask;  // persistent: one CTA per SM over the (unit, key cube) tasks of the range
     int* ctr = store_ds ? reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + ((tiles * (8192 + 4) + 15) & ~int64_t(15)))
                         : nullptr;
     if (ctr) cudaMemsetAsync(ctr, 0, sizeof(int), st);
     kern<<<unsigned(std::min<int64_t>(ntasks, sms)), kKVThreads, smem, st>>>(
-        tq, tk, tv, tdo, L, int(ntasks), int(top_k), scale, scale_log2, lse, delta, offs, idx,
+        tq, tk, tv, tdo, L, int(task_begin), int(ntasks), int(top_k), scale, scale_log2, lse, delta, offs, idx,
                                          dkc, dvc, raster, static_cast<__nv_bfloat16*>(dk),
                                          static_cast<__nv_bfloat16*>(dv), tds, pos, store_ds ? 1 : 0, ctr,
                                          debug_trace());
@@ -1150,7 +1158,7 @@ static int bwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
     const size_t smem = DQCfg<D>::kTiles + sizeof(DQSmall) + 1024;
     auto kern = fine_dq_gemm_sm100_kernel<D>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    kern<<<grid, kDQThreads, smem, st>>>(tk, tds, L, int(top_k), scale, sel, dqc, raster,
+    kern<<<grid, kDQThreads, smem, st>>>(tk, tds, L, 0, int(top_k), scale, sel, dqc, raster,
                                         static_cast<__nv_bfloat16*>(dq));
     return kernel_status("fine_dq_gemm_sm100_kernel");
   }
@@ -1166,12 +1174,13 @@ int launch_fine_backward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, con
                                const void* v, const void* dof, const float* lse, const float* delta,
                                const int32_t* sel, int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx,
                                const float* dqc, const float* dkc, const float* dvc, int32_t raster, void* dq,
-                               void* dk, void* dv, void* ws, size_t ws_bytes, cudaStream_t st) {
+                               void* dk, void* dv, void* ws, size_t ws_bytes, int64_t task_begin, int64_t task_end,
+                               cudaStream_t st) {
   if (d == 128)
     return bwd_launch<128>(L, bh, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc, dvc, raster,
-                           dq, dk, dv, ws, ws_bytes, st);
+                           dq, dk, dv, ws, ws_bytes, task_begin, task_end, st);
   return bwd_launch<64>(L, bh, q, k, v, dof, lse, delta, sel, top_k, selT_offs, selT_idx, dqc, dkc, dvc, raster, dq,
-                        dk, dv, ws, ws_bytes, st);
+                        dk, dv, ws, ws_bytes, task_begin, task_end, st);
 }
 
 }  // namespace vsa_host

@@ -14,7 +14,9 @@
 // SWIZZLE_128B tiles, read K-major for S^T and MN-major (transposed, no copy) for O^T.
 // P^T is written by the softmax threads straight into the MN-major SW128 layout.
 //
-// Persistent, one CTA per SM, query cubes t = blockIdx.x + j*gridDim.x. The pair
+// Persistent, one CTA per SM, query cubes t = task0 + blockIdx.x + j*gridDim.x (task0 /
+// ntasks: a contiguous (unit, query cube) range, the whole problem or a rank's share of
+// a sub-split head). The pair
 // stream is global across the CTA's query cubes: a ring of NG granules (one pair of
 // K or V cubes each) is kept filled by the producer warp across cube boundaries, so
 // the L2->SMEM stream never drains (the kernel is bound by that stream: 64 KB per
@@ -163,7 +165,7 @@ __device__ __forceinline__ int rs_q0(int lane) {
 template <int D>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     fine_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                          const __grid_constant__ CUtensorMap tm_v, DevLayout L, int ntasks, int k_sel,
+                          const __grid_constant__ CUtensorMap tm_v, DevLayout L, int task0, int ntasks, int k_sel,
                           float scale_log2, float tau, const int32_t* __restrict__ sel, __nv_bfloat16* __restrict__ of,
                           float* __restrict__ lse, float* __restrict__ rmax, const __nv_bfloat16* __restrict__ gc,
                           const __nv_bfloat16* __restrict__ gf, const float* __restrict__ oc, int flags,
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       int item = 0;
       unsigned long long tiles = 0;  // executed (query cube, key cube) tiles (MacCounter, fine.hpp:59-63)
       for (int j = 0; j < ntask_local; ++j) {
-        const int t = int(blockIdx.x) + j * ncta;
+        const int t = task0 + int(blockIdx.x) + j * ncta;
         const int64_t u = t / L.nc;
         const int qc = t - int(u) * L.nc;
         const int row0 = int(u * L.seqp);
@@ -358,7 +360,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // mask pad: the key cubes of this query cube's pairs (for the padded-key test)
       const int32_t* mrow_sel = nullptr;
       if (L.mask) {
-        const int t = int(blockIdx.x) + j * ncta;
+        const int t = task0 + int(blockIdx.x) + j * ncta;
         mrow_sel = sel + int64_t(t) * k_sel;  // t = u * nc + qc
       }
 #pragma unroll
@@ -509,7 +511,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                adapt = flags & VSA_FINE_ADAPTATION;
     const float kLn2 = 0.6931471805599453f;
     for (int j = 0; j < ntask_local; ++j) {
-      const int t = int(blockIdx.x) + j * ncta;
+      const int t = task0 + int(blockIdx.x) + j * ncta;
       const int64_t u = t / L.nc;
       const int qc = t - int(u) * L.nc;
       const int row0 = int(u * L.seqp);
@@ -604,7 +606,8 @@ bool sm100_fine_supported(const vsa_layout_t& L, int64_t d, int32_t dtype) {
 template <int D>
 static int fwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const void* k, const void* v,
                       const int32_t* sel, int64_t top_k, void* o_fine, float* lse, float* row_max, const void* gc,
-                      const void* gf, const float* oc_cube, int32_t flags, void* out, cudaStream_t st) {
+                      const void* gf, const float* oc_cube, int32_t flags, void* out, int64_t task_begin,
+                      int64_t task_end, cudaStream_t st) {
   using C = FwdCfg<D>;
   CUtensorMap tq, tk, tv;
   const uint64_t rows = uint64_t(bh * Lh.seq_padded);
@@ -618,7 +621,7 @@ static int fwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const float scale_log2 = (1.0f / std::sqrt(float(D))) * 1.4426950408889634f;
   const float tau = row_max ? 0.f : 8.f;
-  const int64_t ntasks = bh * Lh.nc;
+  const int64_t ntasks = task_end - task_begin;  // (unit, query cube) tasks of this launch
   if (bh * std::max<int64_t>(Lh.seq, Lh.seq_padded) >= (int64_t(1) << 31)) {
     set_error("fine_forward: more than 2^31 token rows");
     return VSA_EINVAL;
@@ -627,7 +630,8 @@ static int fwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = unsigned(std::min<int64_t>(ntasks, sms));  // persistent: one CTA per SM
-  kern<<<grid, kFwdThreads, smem, st>>>(tq, tk, tv, to_dev(Lh), int(ntasks), int(top_k), scale_log2, tau, sel,
+  kern<<<grid, kFwdThreads, smem, st>>>(tq, tk, tv, to_dev(Lh), int(task_begin), int(ntasks), int(top_k), scale_log2,
+                                       tau, sel,
                                        static_cast<__nv_bfloat16*>(o_fine), lse, row_max,
                                        static_cast<const __nv_bfloat16*>(gc), static_cast<const __nv_bfloat16*>(gf),
                                        oc_cube, flags, static_cast<__nv_bfloat16*>(out), debug_trace(),
@@ -638,10 +642,12 @@ static int fwd_launch(const vsa_layout_t& Lh, int64_t bh, const void* q, const v
 int launch_fine_forward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, const void* q, const void* k,
                               const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse,
                               float* row_max, const void* gc, const void* gf, const float* oc_cube, int32_t flags,
-                              void* out, cudaStream_t st) {
+                              void* out, int64_t task_begin, int64_t task_end, cudaStream_t st) {
   if (d == 128)
-    return fwd_launch<128>(L, bh, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube, flags, out, st);
-  return fwd_launch<64>(L, bh, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube, flags, out, st);
+    return fwd_launch<128>(L, bh, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube, flags, out, task_begin,
+                           task_end, st);
+  return fwd_launch<64>(L, bh, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube, flags, out, task_begin,
+                        task_end, st);
 }
 
 }  // namespace vsa_host

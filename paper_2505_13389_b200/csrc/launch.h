@@ -91,12 +91,13 @@ bool sm100_fine_bwd_supported(const vsa_layout_t& L, int64_t d, int32_t dtype);
 int launch_fine_forward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, const void* q, const void* k,
                               const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse,
                               float* row_max, const void* gc, const void* gf, const float* oc_cube, int32_t flags,
-                              void* out, cudaStream_t st);
+                              void* out, int64_t task_begin, int64_t task_end, cudaStream_t st);
 int launch_fine_backward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, const void* q, const void* k,
                                const void* v, const void* dof, const float* lse, const float* delta,
                                const int32_t* sel, int64_t top_k, const int32_t* selT_offs, const int32_t* selT_idx,
                                const float* dqc, const float* dkc, const float* dvc, int32_t raster, void* dq,
-                               void* dk, void* dv, void* ws, size_t ws_bytes, cudaStream_t st);
+                               void* dk, void* dv, void* ws, size_t ws_bytes, int64_t task_begin, int64_t task_end,
+                               cudaStream_t st);
 size_t fine_backward_ws_bytes(const vsa_layout_t& L, int64_t bh, int64_t top_k);
 
 }  // namespace vsa_host

@@ -103,6 +103,7 @@ struct vsa_op {
   const int32_t* fine_sel = nullptr;
   int64_t fine_k = 0;
   bool have_fwd = false;
+  bool have_prologue = false;
   int32_t last_bwd_used_ws = 0;
   // stage timing: events [call][stage boundary]
   bool timing = false;
@@ -114,6 +115,8 @@ struct vsa_op {
     return reinterpret_cast<T*>(base + off);
   }
   int64_t bh() const { return desc.batch * desc.heads; }
+  int64_t t0() const { return desc.task_end ? desc.task_begin : 0; }
+  int64_t t1() const { return desc.task_end ? desc.task_end : bh() * layout.nc; }
 };
 
 namespace {
@@ -138,6 +141,13 @@ int check_desc(const vsa_layout_t* L, const vsa_op_desc_t* D) {
     VSA_REQUIRE(D->raster, "sequence-major I/O needs raster order");
     VSA_REQUIRE(L->io_batch == D->batch && L->io_heads == D->heads, "sequence-major I/O: layout batch/heads mismatch");
   }
+  const int64_t ntask = D->batch * D->heads * L->nc;
+  VSA_REQUIRE((D->task_begin == 0 && D->task_end == 0) ||
+                  (D->task_begin >= 0 && D->task_begin < D->task_end && D->task_end <= ntask),
+              "vsa_op: task range must be empty (all) or a non-empty part of [0, B*H*nc)");
+  if (D->task_end != 0)
+    VSA_REQUIRE(D->dtype == VSA_BF16 && !(D->flags & VSA_OP_FORCE_SIMT) && D->pool_mode == VSA_POOL_MEAN,
+                "vsa_op: task ranges need the bf16 tcgen05 kernels and mean pooling");
   if (D->dtype == VSA_BF16 && !(D->flags & VSA_OP_FORCE_SIMT))
     VSA_REQUIRE(L->cube == 64 && (D->head_dim == 64 || D->head_dim == 128),
                 "vsa_op: the bf16 tcgen05 path needs 64-token cubes and head_dim 64 or 128 "
@@ -333,9 +343,9 @@ int vsa_op_forward_fine(vsa_op_t* op, const void* gc, const void* gf, void* out,
   cudaStream_t st = as_stream(stream);
   const int32_t flags = VSA_FINE_COMBINE | (D.raster ? VSA_FINE_UNTILE : 0) | (D.adaptation ? VSA_FINE_ADAPTATION : 0) |
                         fine_flags(op);
-  int rc = vsa_fine_forward(&op->layout, op->bh(), D.head_dim, D.dtype, op->q_t, op->k_t, op->v_t, op->fine_sel,
-                            op->fine_k, op->at(p.o_f), op->at<float>(p.lse), nullptr, gc, gf, op->at<float>(p.oc),
-                            flags, out, stream);
+  int rc = vsa_fine_forward_range(&op->layout, op->bh(), D.head_dim, D.dtype, op->q_t, op->k_t, op->v_t,
+                                  op->fine_sel, op->fine_k, op->at(p.o_f), op->at<float>(p.lse), nullptr, gc, gf,
+                                  op->at<float>(p.oc), flags, out, op->t0(), op->t1(), stream);
   if (rc) return rc;
   op->gc = gc;
   op->gf = gf;
@@ -352,11 +362,10 @@ int vsa_op_forward(vsa_op_t* op, const void* q, const void* k, const void* v, co
   return vsa_op_forward_fine(op, gc, gf, out, stream);
 }
 
-int vsa_op_backward(vsa_op_t* op, const void* dout, void* dq, void* dk, void* dv, void* dgc, void* dgf,
-                    void* stream) {
+int vsa_op_backward_prologue(vsa_op_t* op, const void* dout, void* dgc, void* dgf, void* stream) {
   VSA_REQUIRE(op != nullptr, "vsa_op: null op");
   VSA_REQUIRE(op->have_fwd, "vsa_backward: missing or mismatched forward artifacts");
-  VSA_REQUIRE(dout && dq && dk && dv, "vsa_backward: null gradient buffer");
+  VSA_REQUIRE(dout != nullptr, "vsa_backward: null dO");
   const auto& p = op->plan;
   const auto& D = op->desc;
   const vsa_layout_t* L = &op->layout;
@@ -381,14 +390,30 @@ int vsa_op_backward(vsa_op_t* op, const void* dout, void* dq, void* dk, void* dv
                               op->at<float>(p.dvc), op->at<float>(p.scratch), D.coarse, op->at(p.coarse_ws), stream);
   if (rc) return rc;
   record(op, op->ev_b, call, 2, st);
+  op->have_prologue = true;
+  return VSA_OK;
+}
+
+int vsa_op_backward_finish(vsa_op_t* op, void* dq, void* dk, void* dv, void* stream) {
+  VSA_REQUIRE(op != nullptr, "vsa_op: null op");
+  VSA_REQUIRE(op->have_prologue, "vsa_backward: finish before the prologue");
+  VSA_REQUIRE(dq && dk && dv, "vsa_backward: null gradient buffer");
+  const auto& p = op->plan;
+  const auto& D = op->desc;
+  const vsa_layout_t* L = &op->layout;
+  const int64_t bh = op->bh(), d = D.head_dim;
+  const int32_t raster = D.raster ? 1 : 0;
+  cudaStream_t st = as_stream(stream);
   const bool mean = D.pool_mode == VSA_POOL_MEAN;
   const size_t need = vsa_fine_backward_workspace_bytes(L, bh, op->fine_k);
-  const bool use_ws = !(D.flags & VSA_OP_NO_DS_WORKSPACE) && op->ws != nullptr && op->ws_bytes >= need;
-  rc = vsa_fine_backward(L, bh, d, D.dtype, op->q_t, op->k_t, op->v_t, op->at(p.dof), op->at<float>(p.lse),
-                         op->at<float>(p.delta), op->fine_sel, op->fine_k, op->at<int32_t>(p.selT_offs),
-                         op->at<int32_t>(p.selT_idx), mean ? op->at<float>(p.dqc) : nullptr,
-                         mean ? op->at<float>(p.dkc) : nullptr, mean ? op->at<float>(p.dvc) : nullptr, raster,
-                         fine_flags(op), dq, dk, dv, use_ws ? op->ws : nullptr, use_ws ? op->ws_bytes : 0, stream);
+  const bool use_ws = !(D.flags & VSA_OP_NO_DS_WORKSPACE) && op->ws != nullptr && op->ws_bytes >= need &&
+                      D.task_end == 0;
+  int rc = vsa_fine_backward_range(L, bh, d, D.dtype, op->q_t, op->k_t, op->v_t, op->at(p.dof), op->at<float>(p.lse),
+                                   op->at<float>(p.delta), op->fine_sel, op->fine_k, op->at<int32_t>(p.selT_offs),
+                                   op->at<int32_t>(p.selT_idx), mean ? op->at<float>(p.dqc) : nullptr,
+                                   mean ? op->at<float>(p.dkc) : nullptr, mean ? op->at<float>(p.dvc) : nullptr,
+                                   raster, fine_flags(op), dq, dk, dv, use_ws ? op->ws : nullptr,
+                                   use_ws ? op->ws_bytes : 0, op->t0(), op->t1(), stream);
   if (rc) return rc;
   op->last_bwd_used_ws = use_ws ? 1 : 0;
   if (!mean) {  // max pooling: route the cube grads to the first argmax tokens (coarse.hpp:172-176)
@@ -400,9 +425,19 @@ int vsa_op_backward(vsa_op_t* op, const void* dout, void* dq, void* dk, void* dv
       if (rc) return rc;
     }
   }
-  record(op, op->ev_b, call, 3, st);
+  record(op, op->ev_b, op->nb, 3, st);
   if (op->timing) ++op->nb;
+  op->have_prologue = false;
   return VSA_OK;
+}
+
+int vsa_op_backward(vsa_op_t* op, const void* dout, void* dq, void* dk, void* dv, void* dgc, void* dgf,
+                    void* stream) {
+  VSA_REQUIRE(op != nullptr, "vsa_op: null op");
+  VSA_REQUIRE(dout && dq && dk && dv, "vsa_backward: null gradient buffer");
+  int rc = vsa_op_backward_prologue(op, dout, dgc, dgf, stream);
+  if (rc) return rc;
+  return vsa_op_backward_finish(op, dq, dk, dv, stream);
 }
 
 int vsa_forward(vsa_op_t* op, const void* hidden, const void* gate_weight, const float* gate_bias, const void* q,

@@ -114,3 +114,74 @@ def test_ulysses_two_ranks_bitwise():
         p.join(timeout=60)
     for r in range(2):
         assert res[r] == "ok", res[r]
+
+
+class _SimExchange:
+    """In-process stand-in for the all-reduce of SubSplitVsa (threads share one GPU):
+    every rank adds its [units*Lp] buffer into one accumulator, waits for all, reads it back."""
+
+    def __init__(self, world):
+        import threading
+
+        self.world, self.acc, self.lock = world, None, threading.Lock()
+        self.b1, self.b2 = threading.Barrier(world, timeout=300), threading.Barrier(world, timeout=300)
+
+    def __call__(self, buf):
+        torch.cuda.synchronize()
+        with self.lock:
+            self.acc = buf.clone() if self.acc is None else self.acc + buf
+        self.b1.wait()
+        torch.cuda.synchronize()
+        buf.copy_(self.acc)
+        torch.cuda.synchronize()
+        if self.b2.wait() == 0:  # one thread resets the accumulator once everyone has read it
+            self.acc = None
+
+
+@pytest.mark.parametrize("world", [2, 5, 8])
+def test_cube_subsplit_bitwise(vsa, world):
+    """SubSplitVsa (heads shared between ranks, lse / delta exchanged): every rank's rows of
+    out (its query cubes), dq (its query cubes), dk / dv (its key cubes) are bitwise equal to
+    one operator on the whole problem (the recompute-dQ backward, which the sub-split uses)."""
+    import threading
+
+    from paper_2505_13389_b200.partition import SubSplitVsa
+
+    L = vsa.TileLayout(8, 16, 16)  # nc = 32, tile order: a task's rows are contiguous
+    B, H, d, k = 1, 3, 128, 6
+    g = torch.Generator(device="cuda").manual_seed(12)
+    xs = [torch.randn((B, H, L.seq_padded, d), generator=g, device="cuda").bfloat16() for _ in range(6)]
+    full = vsa.VsaOp(L, B, H, d, k, raster=False, bwd_workspace=False)
+    ref = [full.forward(*xs[:5]).clone()] + [t.clone() for t in full.backward(xs[5])]
+    torch.cuda.synchronize()
+    ex = _SimExchange(world)
+    parts = [SubSplitVsa(L, B, H, d, k, r, world, exchange=ex, raster=False) for r in range(world)]
+    res = [None] * world
+
+    def run(r):
+        p = parts[r]
+        sh = [p.shard(x).contiguous() for x in xs]
+        out = p.forward(*sh[:5])
+        grads = p.backward(sh[5])
+        torch.cuda.synchronize()
+        res[r] = [out] + list(grads)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    Lp, nc = L.seq_padded, L.num_cubes
+    flat_ref = [x.reshape(-1, d) for x in ref]
+    covered = 0
+    for p, r in zip(parts, res):
+        lo, hi = p.t0 * 64, p.t1 * 64  # global tiled rows of this rank's tasks
+        off = p.ua * Lp
+        for i in (0, 1, 2, 3):  # out, dq (query cubes) and dk, dv (key cubes) of the range
+            got = r[i].reshape(-1, d)[lo - off:hi - off]
+            assert torch.equal(got, flat_ref[i][lo:hi]), f"rank tasks [{p.t0},{p.t1}) output {i}"
+        covered += hi - lo
+        assert p.n <= 2
+    assert covered == B * H * Lp
+    # the shared heads really are split: some rank starts mid-head
+    assert any(p.t0 % nc for p in parts)
