@@ -104,16 +104,9 @@ __global__ void __launch_bounds__(128) coarse_softmax_topk_kernel(int64_t rows, 
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int b = lane; b < 256; b += 32) hist[b] = 0;
     __syncwarp();
-    // warp-aggregated histogram: probabilities of one row share most high bits (the first
-    // passes put nearly every element in one bin), so lanes with equal bins are grouped with
-    // match.any and one leader adds the group size (no 32-way serialised shared atomics)
-    for (int base = 0; base < nc; base += 32) {
-      const int j = base + lane;
-      const uint32_t b = j < nc ? vals[j] : 0u;
-      const bool act = j < nc && (b & mask) == prefix;
-      const uint32_t key = act ? ((b >> shift) & 255u) : 0x100u;
-      const uint32_t peers = __match_any_sync(0xffffffffu, key);
-      if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[key], uint32_t(__popc(peers)));
+    for (int j = lane; j < nc; j += 32) {
+      const uint32_t b = vals[j];
+      if ((b & mask) == prefix) atomicAdd(&hist[(b >> shift) & 255u], 1u);
     }
     __syncwarp();
     // lane l owns bins [255-8l .. 248-8l] (descending); suffix counts from the top

@@ -24,7 +24,9 @@ struct TilePoolArgs {
 
 // grid.x: groups of `cpb` cubes over bh*nc, grid.y: tensor index.
 // in_tiled: input already tile-ordered (pool only).
-template <typename T>
+// MASK: the mask-pad mode (padded tokens excluded from the pool); a template flag so the
+// default path carries no per-token validity test.
+template <typename T, bool MASK>
 __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh, int d, TilePoolArgs<T> a,
                                                         int pool_mode, int in_tiled) {
   constexpr int V = Vec<T>::N;
@@ -74,13 +76,13 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
         if (xt) *reinterpret_cast<uint4*>(xt + (tile_base + o) * d + ch * V) = raw[b];
         float v[V];
         load16(reinterpret_cast<const T*>(&raw[b]), v);
-        if (L.mask && !tile_token_valid(L, c, o)) continue;  // mask pad: padded tokens are not pooled
+        if (MASK && !tile_token_valid(L, c, o)) continue;  // mask pad: padded tokens are not pooled
         if (pool_mode != VSA_POOL_MAX) {  // mean, or the internal sum mode
 #pragma unroll
           for (int i = 0; i < V; ++i) acc[i] = acc[i] + v[i];
         } else {
 #pragma unroll
-          for (int i = 0; i < V; ++i) acc[i] = first ? v[i] : fmaxf_ordered(acc[i], v[i]);
+          for (int i = 0; i < V; ++i) acc[i] = (MASK ? first : o == 0) ? v[i] : fmaxf_ordered(acc[i], v[i]);
         }
         first = false;
       }
@@ -102,13 +104,13 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
           for (int i = 0; i < V; ++i) v[i] = 0.f;
         }
         if (xt) store16(xt + (tile_base + o) * d + ch * V, v);
-        if (L.mask && !tile_token_valid(L, c, o)) continue;
+        if (MASK && !tile_token_valid(L, c, o)) continue;
         if (pool_mode != VSA_POOL_MAX) {  // mean, or the internal sum mode
 #pragma unroll
           for (int i = 0; i < V; ++i) acc[i] = acc[i] + v[i];
         } else {
 #pragma unroll
-          for (int i = 0; i < V; ++i) acc[i] = first ? v[i] : fmaxf_ordered(acc[i], v[i]);
+          for (int i = 0; i < V; ++i) acc[i] = (MASK ? first : o == 0) ? v[i] : fmaxf_ordered(acc[i], v[i]);
         }
         first = false;
       }
@@ -162,7 +164,10 @@ static int launch_tile_pool_t(const vsa_layout_t& Lh, int64_t bh, int64_t d, int
   const int cpb = 128 / chunks;
   const int64_t groups = (bh * Lh.nc + cpb - 1) / cpb;
   dim3 grid{unsigned(groups), unsigned(n), 1u};
-  tile_pool_kernel<T><<<grid, cpb * chunks, 0, st>>>(to_dev(Lh), bh, int(d), a, pool_mode, in_tiled);
+  if (Lh.pad_mode == VSA_PAD_MASK)
+    tile_pool_kernel<T, true><<<grid, cpb * chunks, 0, st>>>(to_dev(Lh), bh, int(d), a, pool_mode, in_tiled);
+  else
+    tile_pool_kernel<T, false><<<grid, cpb * chunks, 0, st>>>(to_dev(Lh), bh, int(d), a, pool_mode, in_tiled);
   VSA_LAUNCH_CHECK("tile_pool_kernel");
 }
 
