@@ -1,5 +1,7 @@
 # SPDX-License-Identifier: Apache-2.0
-"""Debug: pipeline event trace of one persistent fine-forward CTA (Wan2.1-1.3B shape)."""
+"""Debug: pipeline event trace of one persistent fine-forward CTA. Needs the library built
+with -DVSA_TRACE (tools/build_variant.sh trace fine_fwd_sm100.cu -DVSA_TRACE, then
+VSA_LIB_PATH=.../libvsa_trace.so). usage: trace_fwd.py [wan13|dit]"""
 import ctypes as C
 import sys
 
@@ -8,10 +10,12 @@ import torch
 sys.path.insert(0, ".")
 import paper_2505_13389_b200 as vsa  # noqa: E402
 
-L = vsa.TileLayout(21, 30, 52, pad=True)
-op = vsa.VsaOp(L, 1, 12, 128, 78)
+cfg = sys.argv[1] if len(sys.argv) > 1 else "wan13"
+grid, B, H, d, k = {"wan13": ((21, 30, 52), 1, 12, 128, 78), "dit": ((16, 32, 32), 8, 16, 64, 32)}[cfg]
+L = vsa.TileLayout(*grid, pad=True)
+op = vsa.VsaOp(L, B, H, d, k)
 g = torch.Generator(device="cuda").manual_seed(1)
-x = [torch.randn((1, 12, L.seq_len, 128), generator=g, device="cuda").bfloat16() for _ in range(5)]
+x = [torch.randn((B, H, L.seq_len, d), generator=g, device="cuda").bfloat16() for _ in range(5)]
 for _ in range(2):
     op.forward(*x)
 torch.cuda.synchronize()
