@@ -673,6 +673,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: VSA_BENCH_BACKEND=gloo runs several ranks on the visible GPUs (ranks share a
+    # device when there are fewer GPUs than ranks); the product path is NCCL, one GPU per rank
+    backend = os.environ.get("VSA_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        import torch
+
+        local_rank = local_rank % max(1, torch.cuda.device_count())
     if args.impl == "reference":
         line = run_reference(args, rank, world)
         if line is not None:
@@ -683,7 +690,10 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         line = (run_sp if CONFIGS[args.config].get("sp") else run_ours)(args, rank, world, local_rank)
         if line is not None:
