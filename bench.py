@@ -339,7 +339,8 @@ def run_ours(args, rank, world, local_rank):
     if not split:
         del op  # free the resident-input operator's buffers before building the pipeline
         torch.cuda.empty_cache()
-    pipe = (vsa.VsaHostPipeline(L, 1, n, d, K, chunks=min(args.e2e_chunks, n), dtype=dtype) if n and not split
+    pipe = (vsa.VsaHostPipeline(L, 1, n, d, K, chunks=min(args.e2e_chunks, n), dtype=dtype, slots=args.e2e_slots)
+            if n and not split
             else None)
     if split:  # the sub-split op stays; its inputs come from host every step
         op = part.op
@@ -664,7 +665,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=12, help="host-pipeline unit groups for the e2e leg")
+    ap.add_argument("--e2e-chunks", type=int, default=6, help="host-pipeline unit groups for the e2e leg")
+    ap.add_argument("--e2e-slots", type=int, default=3, help="host-pipeline device buffer slots for the e2e leg")
     ap.add_argument("--coarse", default="fp32", choices=["fp32", "bf16"],
                     help="coarse-stage mode of the headline op: fp32 (bit-exact block map) or bf16 (tcgen05)")
     args = ap.parse_args()

@@ -659,80 +659,86 @@ class VsaHostPipeline:
 
     Every (b, h) unit is independent (fine.hpp:65,129,172), so the B*H units are
     split into `chunks` groups; group i+1 is copied in on one stream while group
-    i computes, and group i-1 is copied out on a third — double-buffered device
-    inputs/outputs, events for the hand-offs. Result == VsaOp on the whole batch.
+    i computes, and group i-1 is copied out on a third — `slots`-deep device
+    input/output buffers, events for the hand-offs. Result == VsaOp on the whole batch.
+
+    The copies are released at the operator's stage boundaries, so the PCIe fill
+    and drain around the first and last group are as short as the data allows:
+    q / k / v land before the gates (K1-K3 need only q / k / v; the gates are first
+    read by the fine forward's combine), dO after them; O leaves after the forward,
+    dGc / dGf after the backward prologue (K6a writes them), dQ / dK / dV last.
     """
 
-    def __init__(self, layout: TileLayout, B: int, H: int, d: int, top_k: int, chunks: int = 12,
-                 dtype=torch.bfloat16, device="cuda", **op_kwargs):
+    def __init__(self, layout: TileLayout, B: int, H: int, d: int, top_k: int, chunks: int = 6,
+                 dtype=torch.bfloat16, device="cuda", slots: int = 3, **op_kwargs):
         units = B * H
         chunks = max(1, min(chunks, units))
         self.bounds = [(units * i) // chunks for i in range(chunks + 1)]
         self.units, self.d, self.S, self.dtype = units, d, layout.seq_len, dtype
+        self.slots = max(2, int(slots))
         sizes = sorted({b - a for a, b in zip(self.bounds[:-1], self.bounds[1:])})
         cmax = sizes[-1]
-        # one operator per (group size, buffer slot), built here with the caller's options:
-        # run() never allocates, and ragged groups compute the same operator
-        self.ops = {(c, s): VsaOp(layout, 1, c, d, top_k, dtype=dtype, device=device, **op_kwargs)
-                    for c in sizes for s in range(2)}
+        # one operator per group size, built here with the caller's options: run() never
+        # allocates, and ragged groups compute the same operator. The compute stream runs
+        # the groups in order, so one operator per size serves every buffer slot.
+        self.ops = {c: VsaOp(layout, 1, c, d, top_k, dtype=dtype, device=device, **op_kwargs) for c in sizes}
         e = lambda: torch.empty((1, cmax, self.S, d), dtype=dtype, device=device)
-        self.din = [[e() for _ in range(6)] for _ in range(2)]
-        self.dout = [[e() for _ in range(6)] for _ in range(2)]
+        self.din = [[e() for _ in range(6)] for _ in range(self.slots)]
+        self.dout = [[e() for _ in range(6)] for _ in range(self.slots)]
         self.s_in, self.s_out = torch.cuda.Stream(device), torch.cuda.Stream(device)
         self.h2d_bytes = 6 * units * self.S * d * torch.tensor([], dtype=dtype).element_size()
         self.d2h_bytes = self.h2d_bytes
 
     def run(self, hin, hout):
-        """hin = (q, k, v, gc, gf, dO), hout = (O, dQ, dK, dV, dGc, dGf): pinned host [B,H,S,d].
-
-        Per group: the five forward inputs are copied first and the forward starts as
-        soon as they land (dO follows on the copy stream); O is copied out while the
-        backward runs, the five gradients after it."""
+        """hin = (q, k, v, gc, gf, dO), hout = (O, dQ, dK, dV, dGc, dGf): pinned host [B,H,S,d]."""
         flat = lambda t: t.view(self.units, self.S, self.d)
         hin, hout = [flat(t) for t in hin], [flat(t) for t in hout]
         comp = torch.cuda.current_stream()
-        n = len(self.bounds) - 1
+        n, ns = len(self.bounds) - 1, self.slots
         ev_comp, ev_out = [None] * n, [None] * n
-        ev = lambda: torch.cuda.Event()
+        ev = torch.cuda.Event
+
+        def copy_out(srcs, dsts, a, b, c, after):
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(after)
+                for dst, src in zip(dsts, srcs):
+                    dst[a:b].copy_(src[0, :c], non_blocking=True)
+
         for i in range(n):
             a, b = self.bounds[i], self.bounds[i + 1]
-            c, slot = b - a, i % 2
+            c, slot = b - a, i % ns
             di, do = self.din[slot], self.dout[slot]
+            evs = []
             with torch.cuda.stream(self.s_in):
-                if i >= 2:
-                    self.s_in.wait_event(ev_comp[i - 2])      # slot's inputs consumed
-                for dst, src in zip(di[:5], hin[:5]):
-                    dst[0, :c].copy_(src[a:b], non_blocking=True)
-                ev_fwd_in = ev()
-                ev_fwd_in.record(self.s_in)
-                di[5][0, :c].copy_(hin[5][a:b], non_blocking=True)
-                ev_bwd_in = ev()
-                ev_bwd_in.record(self.s_in)
-            comp.wait_event(ev_fwd_in)
-            if i >= 2:
-                comp.wait_event(ev_out[i - 2])                # slot's outputs drained
-            op = self.ops[(c, slot)]
+                if i >= ns:
+                    self.s_in.wait_event(ev_comp[i - ns])     # slot's inputs consumed
+                for grp in ((0, 1, 2), (3, 4), (5,)):         # q k v | gates | dO
+                    for j in grp:
+                        di[j][0, :c].copy_(hin[j][a:b], non_blocking=True)
+                    evs.append(ev())
+                    evs[-1].record(self.s_in)
+            comp.wait_event(evs[0])
+            if i >= ns:
+                comp.wait_event(ev_out[i - ns])               # slot's outputs drained
+            op = self.ops[c]
             v = lambda t: t[:, :c]  # [1, cmax, S, d] -> [1, c, S, d]: a contiguous prefix view
-            op.forward(*(v(t) for t in di[:5]), out=v(do[0]), check_inputs=False)
+            op.forward(*(v(t) for t in di[:5]), out=v(do[0]), check_inputs=False,
+                       before_fine=lambda: comp.wait_event(evs[1]))
             ev_fwd = ev()
             ev_fwd.record(comp)
-            with torch.cuda.stream(self.s_out):
-                self.s_out.wait_event(ev_fwd)
-                hout[0][a:b].copy_(do[0][0, :c], non_blocking=True)
-            comp.wait_event(ev_bwd_in)
-            op.backward(v(di[5]), *(v(t) for t in do[1:]), check_inputs=False)
-            first_out = 1
+            copy_out(do[:1], hout[:1], a, b, c, ev_fwd)
+            comp.wait_event(evs[2])
+            ev_pro = ev()
+            op.backward(v(di[5]), *(v(t) for t in do[1:]), check_inputs=False,
+                        before_finish=lambda: ev_pro.record(comp))
+            copy_out(do[4:], hout[4:], a, b, c, ev_pro)
             ev_comp[i] = ev()
             ev_comp[i].record(comp)
-            with torch.cuda.stream(self.s_out):
-                self.s_out.wait_event(ev_comp[i])
-                for dst, src in zip(hout[first_out:], do[first_out:]):
-                    dst[a:b].copy_(src[0, :c], non_blocking=True)
-                ev_out[i] = ev()
-                ev_out[i].record(self.s_out)
-        comp.wait_event(ev_out[n - 1])
-        if n >= 2:
-            comp.wait_event(ev_out[n - 2])
+            copy_out(do[1:4], hout[1:4], a, b, c, ev_comp[i])
+            ev_out[i] = ev()
+            ev_out[i].record(self.s_out)
+        for i in range(max(0, n - ns), n):
+            comp.wait_event(ev_out[i])
 
 
 # ----------------------------------------------------------------------------- gate projection (vsa.hpp:100-112)
