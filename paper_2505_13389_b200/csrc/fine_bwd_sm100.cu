@@ -37,6 +37,7 @@
 // and epilogue costs (~9000 cycles per key cube) are gone; the dynamic hand-out keeps
 // the very uneven list lengths of the transposed map balanced.
 #include <cmath>
+#include <type_traits>
 
 #include "common.cuh"
 #include "launch.h"
@@ -165,6 +166,23 @@ struct GranSeq {
   }
 };
 
+// d = 64 (kMergeGK): Q(p) and dO(p) share one double granule m = p % (NG / 2), dO in
+// granule 2m and Q in 2m + 1, both released by the merged dV / dK product of pair p, so
+// the ring is handed out in pair order.
+template <int NG>
+struct PairSeq {
+  int m = 0;
+  __device__ __forceinline__ int next(int i) {
+    const int g = (i & 1) ? 2 * m : 2 * m + 1;  // item 2p = Q(p), 2p + 1 = dO(p)
+    if (i & 1) m = (m + 1 == NG / 2) ? 0 : m + 1;
+    return g;
+  }
+};
+
+#ifndef VSA_DKDV_MERGE
+#define VSA_DKDV_MERGE 1
+#endif
+
 template <int D>
 struct KVCfg {
   static constexpr int kChunks = D / 64;
@@ -181,8 +199,18 @@ struct KVCfg {
   static constexpr int kTiles = kOffZ + (D == 64 ? 16384 : 0);
   static constexpr int kPairChunk = 16384;  // 128 rows x 128 B
   static constexpr int kCubeChunk = 8192;   // 64 rows x 128 B
+  // d = 64: dV^T and dK^T in ONE M = 128, N = 128 product per K-step,
+  //   [dV^T  . ]   [dO^T]
+  //   [ .  dK^T] = [Q^T ] . [P | dS]
+  // (the off-diagonal blocks are discarded): 8 KB of SMEM operands per 64-cycle MMA,
+  // the full tensor rate, against two N = 64 products each capped at 2/3 by their 6 KB
+  // (profiles/mma_issue_bench2_r1.txt). A = dO^T with Q^T at LBO (adjacent granules), B =
+  // P with dS at LBO (adjacent buffers).
+  static constexpr bool kMergeGK = D == 64 && VSA_DKDV_MERGE != 0;
   static_assert(kTiles <= 225 * 1024, "dK/dV smem budget");
 };
+template <int D>
+using KVSeq = typename std::conditional<KVCfg<D>::kMergeGK, PairSeq<KVCfg<D>::kNG>, GranSeq<KVCfg<D>::kNG>>::type;
 
 constexpr int kTaskRing = 8;
 // task-ring readers: dS-store thread, watcher, issuer, 8 compute warps, 4 epilogue warps
@@ -337,7 +365,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_do);
-      GranSeq<NG> seq;
+      KVSeq<D> seq;
       uint32_t fills = 0;  // bit g: parity of the fills of granule g so far
       int i = 0, kvn = 0;  // global item index, non-empty tasks so far
       for (int j = 0;; ++j) {
@@ -380,7 +408,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kKVRegCtl));
     // load watcher: waits for each streamed granule's TMA (and each task's K / V), then
     // meets the issuer at a named barrier, in consumption order
-    GranSeq<NG> seq;
+    KVSeq<D> seq;
     uint32_t fills = 0;
     int i = 0, kvn = 0;
     for (int j = 0;; ++j) {
@@ -409,8 +437,11 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     const uint64_t dK0 = make_sdesc_sw128(smem_u32(sK), 16, 1024), dV0 = make_sdesc_sw128(smem_u32(sV), 16, 1024);
     const uint64_t dG0 = make_sdesc_sw128(aG, 16, 1024);
     const uint64_t dP0 = make_sdesc_sw128(aP, 8192, 1024), dS0 = make_sdesc_sw128(aS, 8192, 1024);
+    // merged dV / dK (d = 64): B = [P | dS], the second N block (dS) at LBO
+    const uint64_t dPS0 = make_sdesc_sw128(aP, aS - aP, 1024);
+    constexpr uint32_t idGK = make_idesc_bf16(128, 128, true, true);
     const uint32_t lboZ = (D == 128) ? uint32_t(C::kPairChunk) : smem_u32(sZ) - aG;  // minus granule offset
-    GranSeq<NG> seq;
+    KVSeq<D> seq;
     // granules of Q / dO of the two pairs in flight, by pair parity (scalars: a
     // runtime-indexed array would live in local memory, whose loads the SS MMA
     // operand stream starves). The issuing warp runs nearly in lock-step with the
@@ -453,42 +484,70 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       const int ab = acn & 1;
       const uint32_t tV = tbase + 256 + ab * 128, tK = tV + 64;  // this task's dV^T / dK^T accumulators
       if (lane == 0) trace_ev(tr, 12, j);
-      // Fixed software-pipelined order per pair p:  S(p+1), dV(p), dP(p+1), dK(p).
-      // The exp / dS math of a pair runs a full period ahead of its dV / dK. K / V of
-      // the next task are released after the last dP (kv_empty), so their load
-      // overlaps this task's last dV / dK groups.
-      issue_s(P);
-      issue_dp(P);
-      if (npairs == 1) umma_commit_warp(&sm->kv_empty);
-      for (int p = 0; p < npairs; ++p) {
-        const int n = P + p, b = n & 1;
-        if (p + 1 < npairs) issue_s(n + 1);
-        {
-          const int g = b ? go1 : go0;
-          const uint32_t goff = uint32_t(g * C::kGran);
-          const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
-          if (p == 0 && acn >= 2) mbar_wait_warp(&sm->acc_free[ab], ((acn >> 1) & 1) ^ 1);  // epilogue of task-2 read it
+      if constexpr (C::kMergeGK) {
+        // d = 64, per pair p: S(p+1), dP(p+1), then the merged dV / dK product G(p) once
+        // P(p) and dS(p) are written; the tensor pipe runs S / dP of the next pair while
+        // the compute warps produce dS(p).
+        issue_s(P);
+        issue_dp(P);
+        if (npairs == 1) umma_commit_warp(&sm->kv_empty);
+        for (int p = 0; p < npairs; ++p) {
+          const int n = P + p, b = n & 1;
+          if (p + 1 < npairs) {
+            issue_s(n + 1);
+            issue_dp(n + 1);
+            if (p + 2 == npairs) umma_commit_warp(&sm->kv_empty);
+          }
+          const int go = b ? go1 : go0, gq = b ? gq1 : gq0;  // dO(n) in 2m, Q(n) in 2m + 1
+          const uint64_t da = make_sdesc_sw128(aG + uint32_t(go * C::kGran), uint32_t(C::kGran), 1024);
+          if (p == 0 && acn >= 2) mbar_wait_warp(&sm->acc_free[ab], ((acn >> 1) & 1) ^ 1);
           named_bar_b(kBarPFull, kCompute + 32);
-          tc_fence_after();
-#pragma unroll
-          for (int s = 0; s < 8; ++s)
-            umma_bf16_warp(tV, da + uint64_t(s * 128), dP0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
-          umma_commit_warp(&sm->g_empty[g]);
-        }
-        if (p + 1 < npairs) {
-          issue_dp(n + 1);
-          if (p + 2 == npairs) umma_commit_warp(&sm->kv_empty);
-        }
-        {
-          const int g = b ? gq1 : gq0;
-          const uint32_t goff = uint32_t(g * C::kGran);
-          const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
           named_bar_b(kBarDsFull, kCompute + 32);
           tc_fence_after();
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_bf16_warp(tK, da + uint64_t(s * 128), dS0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
-          umma_commit_warp(&sm->g_empty[g]);
+            umma_bf16_warp(tV, da + uint64_t(s * 128), dPS0 + uint64_t(s * 128), idGK, (p > 0 || s > 0) ? 1u : 0u);
+          umma_commit_warp(&sm->g_empty[go]);
+          umma_commit_warp(&sm->g_empty[gq]);
+        }
+      } else {
+        // Fixed software-pipelined order per pair p:  S(p+1), dV(p), dP(p+1), dK(p).
+        // The exp / dS math of a pair runs a full period ahead of its dV / dK. K / V of
+        // the next task are released after the last dP (kv_empty), so their load
+        // overlaps this task's last dV / dK groups.
+        issue_s(P);
+        issue_dp(P);
+        if (npairs == 1) umma_commit_warp(&sm->kv_empty);
+        for (int p = 0; p < npairs; ++p) {
+          const int n = P + p, b = n & 1;
+          if (p + 1 < npairs) issue_s(n + 1);
+          {
+            const int g = b ? go1 : go0;
+            const uint32_t goff = uint32_t(g * C::kGran);
+            const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
+            if (p == 0 && acn >= 2) mbar_wait_warp(&sm->acc_free[ab], ((acn >> 1) & 1) ^ 1);  // epilogue of task-2 read it
+            named_bar_b(kBarPFull, kCompute + 32);
+            tc_fence_after();
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+              umma_bf16_warp(tV, da + uint64_t(s * 128), dP0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+            umma_commit_warp(&sm->g_empty[g]);
+          }
+          if (p + 1 < npairs) {
+            issue_dp(n + 1);
+            if (p + 2 == npairs) umma_commit_warp(&sm->kv_empty);
+          }
+          {
+            const int g = b ? gq1 : gq0;
+            const uint32_t goff = uint32_t(g * C::kGran);
+            const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
+            named_bar_b(kBarDsFull, kCompute + 32);
+            tc_fence_after();
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+              umma_bf16_warp(tK, da + uint64_t(s * 128), dS0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+            umma_commit_warp(&sm->g_empty[g]);
+          }
         }
       }
       umma_commit_warp(&sm->acc_full[ab]);
@@ -505,7 +564,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     // thread reads its d row in 32-column slices and stores bf16 scalars (one warp
     // instruction = 64 contiguous bytes of a token row), adding the cube-level
     // mean-unpool term; the whole epilogue overlaps the next task's products.
-    const int dl = (warp & 3) * 32 + lane;
+    const int dl = C::kMergeGK ? (warp & 1) * 32 + lane : (warp & 3) * 32 + lane;  // d row
     const uint32_t lrow = tbase + (uint32_t((warp & 3) * 32) << 16);
     int acn = 0;
     for (int j = 0;; ++j) {
@@ -523,8 +582,11 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         mbar_wait_sleep(&sm->acc_full[ab], (acn >> 1) & 1);
         tc_fence_after();
       }
+      // merged (d = 64): lanes 0-63 hold dV^T, lanes 64-127 dK^T: warp quadrant q writes
+      // tensor q / 2, rows d = 32 (q % 2) + lane; otherwise every warp writes both.
+      const int t0 = C::kMergeGK ? ((warp & 3) >> 1) : 0, t1 = C::kMergeGK ? t0 + 1 : 2;
 #pragma unroll 1
-      for (int t = 0; t < 2; ++t) {  // t = 0: dV, t = 1: dK
+      for (int t = t0; t < t1; ++t) {  // t = 0: dV, t = 1: dK
         __nv_bfloat16* dst = t ? dk : dv;
         const float sc = t ? scale : 1.f, x = t ? xk : xv;
 #pragma unroll 1
@@ -561,7 +623,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     // The P / dS buffers of pair P-1 are free once dV(P-1) / dK(P-1) complete, which is
     // exactly when the granules of dO(P-1) / Q(P-1) are released: wait on those g_empty
     // phases (same GranSeq as producer / issuer) instead of extra per-pair commits.
-    GranSeq<NG> gseq;
+    KVSeq<D> gseq;
     uint32_t uses = 0;           // bit g: parity of the fills of granule g so far
     int pq_g = 0, po_g = 0;      // granules of Q(P-1), dO(P-1)
     uint32_t pq_par = 0, po_par = 0;
