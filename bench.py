@@ -404,6 +404,20 @@ def run_ours(args, rank, world, local_rank):
                          for k in ks if k.get("smem_tc_wavefronts_pct")}
         except Exception:
             smem_pipe = None
+    # Second roofline of the fine kernels: the L2 -> SMEM stream of the streamed operand
+    # tiles (selections are random, so a tile's K/V (forward) or Q/dO (dK/dV) and the K + dS
+    # of dQ come from L2 once per selected tile), against the measured chip-wide L2 -> SMEM
+    # TMA rate (profiles/tma_bench_r1.txt, 2-D 64 x 128 B boxes on all SMs).
+    tiles_r = n_eff * nc * K
+    l2_bytes = {"fine_fwd": tiles_r * 4 * 64 * d,                                    # K, V tiles
+                "fine_bwd": tiles_r * (4 * 64 * d + 8192 + 2 * 64 * d + 8192)}      # Q, dO; dS out; K, dS in
+    l2_peak = 12805.4
+    l2_roof = {"bound": "l2", "unit": "GB/s", "peak": l2_peak,
+               "peak_src": "measured L2->SMEM TMA rate, all SMs (profiles/tma_bench_r1.txt)",
+               "kernels": {s: {"bytes": int(l2_bytes[s]),
+                               "achieved": round(l2_bytes[s] / (max(stage_ms[s], 1e-9) * 1e-3) / 1e9, 1),
+                               "frac": round(l2_bytes[s] / (max(stage_ms[s], 1e-9) * 1e-3) / 1e9 / l2_peak, 4)}
+                           for s in ("fine_fwd", "fine_bwd")}}
     bytes_tp = n * 3 * (S * d * 2 + L.seq_padded * d * 2 + nc * d * 4)  # K1 runs on whole units
     stages = {}
     for s in STAGES:
@@ -449,6 +463,7 @@ def run_ours(args, rank, world, local_rank):
                      "note": "N=64 SS UMMAs are capped at 2/3 of the tensor peak by the 128 B/cycle SMEM "
                              "operand port; smem_pipe_busy_pct = ncu TC + LSU shared wavefronts per kernel "
                              "(profiles/ncu_r1d_kernels.json, DESIGN.md section 4)"},
+        "l2_roofline": l2_roof,
         "stages": stages,
         "dense_baseline": dense,
         "coarse_mode": args.coarse,
