@@ -79,6 +79,9 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
 // waits for the P / dS buffers' release), sd_free alternates by pair parity, and the granule
 // rendezvous is a bar.sync on both sides (pairs up in order on one ID).
 constexpr int kBarPFull = 2, kBarDsFull = 3, kBarSdFree = 4 /* 4,5 */, kBarGran = 6;
+// merged d = 64 path (two {P, dS} buffer pairs: the compute warps may run one pair ahead
+// of the issuer's P / dS rendezvous): one barrier per pair parity
+constexpr int kBarPFullM = 7 /* 7,8 */, kBarDsFullM = 9 /* 9,10 */;
 
 __device__ __forceinline__ void tmem_ld32_raw(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -188,15 +191,24 @@ struct KVCfg {
   static constexpr int kChunks = D / 64;
   static constexpr int kCube = 64 * D * 2;      // one cube
   static constexpr int kGran = 128 * D * 2;     // one pair of cubes of one tensor
-  static constexpr int kNPB = 1;                // P / dS buffers (the issuer assumes 1)
-  static constexpr int kNG = D == 128 ? 5 : 10;  // granules
+  // d = 64 with the merged dV / dK product (kMergeGK, below): 4 double granules and TWO
+  // {P, dS} buffer pairs. With one pair, the compute warps could write dS(p+1) only
+  // after the dS TMA store of pair p had READ dS(p) out of shared memory, which under the
+  // MMA operand stream takes ~1300 cycles (profiles/dkdv_traffic_r1.txt) and paced the
+  // whole pass; the merged product also frees the 16 KB zero tile.
+  static constexpr bool kMerge_ = D == 64 && VSA_DKDV_MERGE != 0;
+  static constexpr int kNPB = kMerge_ ? 2 : 1;   // {P, dS} buffer pairs
+  static constexpr int kNG = D == 128 ? 5 : (kMerge_ ? 8 : 10);  // granules
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + kCube;
   static constexpr int kOffG = kOffV + kCube;
-  static constexpr int kOffP = kOffG + kNG * kGran;     // kNPB x (128 x 128 B)
-  static constexpr int kOffS = kOffP + kNPB * 16384;    // kNPB x (128 x 128 B)
-  static constexpr int kOffZ = kOffS + kNPB * 16384;
-  static constexpr int kTiles = kOffZ + (D == 64 ? 16384 : 0);
+  // P buffer b at kOffP + b * kPBStride, dS buffer b at kOffS + b * kPBStride; the merged
+  // product needs dS right after P (B = [P | dS], dS at LBO = 16 KB)
+  static constexpr int kPBStride = kMerge_ ? 32768 : 16384;
+  static constexpr int kOffP = kOffG + kNG * kGran;
+  static constexpr int kOffS = kOffP + (kMerge_ ? 16384 : kNPB * 16384);
+  static constexpr int kOffZ = kMerge_ ? kOffP + kNPB * 32768 : kOffS + kNPB * 16384;
+  static constexpr int kTiles = kOffZ + (D == 64 && !kMerge_ ? 16384 : 0);
   static constexpr int kPairChunk = 16384;  // 128 rows x 128 B
   static constexpr int kCubeChunk = 8192;   // 64 rows x 128 B
   // d = 64: dV^T and dK^T in ONE M = 128, N = 128 product per K-step,
@@ -206,7 +218,7 @@ struct KVCfg {
   // the full tensor rate, against two N = 64 products each capped at 2/3 by their 6 KB
   // (profiles/mma_issue_bench2_r1.txt). A = dO^T with Q^T at LBO (adjacent granules), B =
   // P with dS at LBO (adjacent buffers).
-  static constexpr bool kMergeGK = D == 64 && VSA_DKDV_MERGE != 0;
+  static constexpr bool kMergeGK = kMerge_;
   static_assert(kTiles <= 225 * 1024, "dK/dV smem budget");
 };
 template <int D>
@@ -303,7 +315,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
   // contents need clearing.
   for (int i = threadIdx.x; i < NG * C::kGran / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(sG)[i] = make_uint4(0, 0, 0, 0);
-  if (D == 64)
+  if (D == 64 && !C::kMergeGK)  // the zero A rows of the unmerged d = 64 dV^T / dK^T products
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) reinterpret_cast<uint4*>(sZ)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
   tc_fence_before();
@@ -344,7 +356,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           const int b = P % NPB;
           mbar_wait(&sm->ds_full[b], (P / NPB) & 1);
           const int e = T.beg + 2 * p;
-          uint8_t* myS = sS + b * 16384;
+          uint8_t* myS = sS + b * C::kPBStride;
           tma_store_2d(&tm_ds, myS, 0, int((base + int64_t(T.list[e]) * k_sel + ds_pos[base + e]) * 64));
           if (2 * p + 1 < T.nq)
             tma_store_2d(&tm_ds, myS + 8192, 0,
@@ -432,7 +444,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     // MMA issuer (whole warp: warp-uniform issue, one elected lane issues)
     constexpr uint32_t idSD = make_idesc_bf16(128, 64, false, false);
     constexpr uint32_t idG = make_idesc_bf16(128, 64, true, true);
-    const uint32_t aG = smem_u32(sG), aP = smem_u32(sP), aS = smem_u32(sS);  // NPB = 1 (static_assert)
+    const uint32_t aG = smem_u32(sG), aP = smem_u32(sP), aS = smem_u32(sS);  // buffer 0 (the unmerged path: NPB = 1)
     // descriptor bases; K-steps advance the start address (+32 B = +2 encoded)
     const uint64_t dK0 = make_sdesc_sw128(smem_u32(sK), 16, 1024), dV0 = make_sdesc_sw128(smem_u32(sV), 16, 1024);
     const uint64_t dG0 = make_sdesc_sw128(aG, 16, 1024);
@@ -501,12 +513,13 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           const int go = b ? go1 : go0, gq = b ? gq1 : gq0;  // dO(n) in 2m, Q(n) in 2m + 1
           const uint64_t da = make_sdesc_sw128(aG + uint32_t(go * C::kGran), uint32_t(C::kGran), 1024);
           if (p == 0 && acn >= 2) mbar_wait_warp(&sm->acc_free[ab], ((acn >> 1) & 1) ^ 1);
-          named_bar_b(kBarPFull, kCompute + 32);
-          named_bar_b(kBarDsFull, kCompute + 32);
+          named_bar_b(kBarPFullM + b, kCompute + 32);
+          named_bar_b(kBarDsFullM + b, kCompute + 32);
           tc_fence_after();
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_bf16_warp(tV, da + uint64_t(s * 128), dPS0 + uint64_t(s * 128), idGK, (p > 0 || s > 0) ? 1u : 0u);
+            umma_bf16_warp(tV, da + uint64_t(s * 128), dPS0 + uint64_t(((n % NPB) * C::kPBStride) >> 4) + uint64_t(s * 128),
+                           idGK, (p > 0 || s > 0) ? 1u : 0u);
           umma_commit_warp(&sm->g_empty[go]);
           umma_commit_warp(&sm->g_empty[gq]);
         }
@@ -627,6 +640,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     uint32_t uses = 0;           // bit g: parity of the fills of granule g so far
     int pq_g = 0, po_g = 0;      // granules of Q(P-1), dO(P-1)
     uint32_t pq_par = 0, po_par = 0;
+    int po2_g = 0;               // granule of dO(P-2) (merged d = 64 path, two buffer pairs)
+    uint32_t po2_par = 0;
     int P = 0;
     for (int j = 0;; ++j) {
       const int t = next_task_warp(j);
@@ -655,8 +670,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const uint32_t co_par = (uses >> co_g) & 1u;
         uses ^= 1u << co_g;
         const int b = P & 1, pb = P % NPB, use = P / NPB;
-        uint8_t* myP = sP + pb * 16384;
-        uint8_t* myS = sS + pb * 16384;
+        uint8_t* myP = sP + pb * C::kPBStride;
+        uint8_t* myS = sS + pb * C::kPBStride;
         const bool valid = ql < 64 || (2 * p + 1 < T.nq);  // warp-uniform
         const float lse2 = nl2 * 1.4426950408889634f, dl = ndl;
         row_stats(p + 1, nl2, ndl);
@@ -687,13 +702,19 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           for (int jj = 0; jj < 16; ++jj) pk[jj] = pack_bf16(pf[2 * jj], pf[2 * jj + 1]);
         }
         if (threadIdx.x == 0) trace_ev(tr, 6, P);
-        if (P >= 1) mbar_wait_sleep(&sm->g_empty[po_g], po_par);  // dV(P-1) done: P buffer free
+        if (C::kMergeGK) {
+          // buffer pair pb was last read by the merged product of pair P-2 (which released
+          // the granules of Q / dO(P-2))
+          if (P >= 2) mbar_wait_sleep(&sm->g_empty[po2_g], po2_par);
+        } else if (P >= 1) {
+          mbar_wait_sleep(&sm->g_empty[po_g], po_par);  // dV(P-1) done: P buffer free
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           *reinterpret_cast<uint4*>(myP + sw128_offset(ql, (ch * 4 + c) * 16)) =
               make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         fence_proxy_async_smem();
-        named_bar_arrive(kBarPFull, kCompute + 32);
+        named_bar_arrive(C::kMergeGK ? kBarPFullM + b : kBarPFull, kCompute + 32);
         mbar_wait_sleep(&sm->dp_full[b], (P >> 1) & 1);
         tc_fence_after();
         {
@@ -712,7 +733,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           }
         }
         if (P >= NPB) {
-          mbar_wait_sleep(&sm->g_empty[pq_g], pq_par);                       // dK(P-1) done: dS buffer free
+          if (!C::kMergeGK) mbar_wait_sleep(&sm->g_empty[pq_g], pq_par);    // dK(P-1) done: dS buffer free
           if (ds_store) mbar_wait_sleep(&sm->ds_stored[pb], (use - 1) & 1);  // and its dS store read it
         }
 #pragma unroll
@@ -720,9 +741,10 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           *reinterpret_cast<uint4*>(myS + sw128_offset(ql, (ch * 4 + c) * 16)) =
               make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         fence_proxy_async_smem();
-        named_bar_arrive(kBarDsFull, kCompute + 32);
+        named_bar_arrive(C::kMergeGK ? kBarDsFullM + b : kBarDsFull, kCompute + 32);
         if (ds_store) mbar_arrive(&sm->ds_full[pb]);  // for the dS store warp
         if (threadIdx.x == 0) trace_ev(tr, 7, P);
+        po2_g = po_g, po2_par = po_par;
         pq_g = cq_g, pq_par = cq_par, po_g = co_g, po_par = co_par;
       }
     }
