@@ -514,7 +514,9 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           const uint64_t da = make_sdesc_sw128(aG + uint32_t(go * C::kGran), uint32_t(C::kGran), 1024);
           if (p == 0 && acn >= 2) mbar_wait_warp(&sm->acc_free[ab], ((acn >> 1) & 1) ^ 1);
           named_bar_b(kBarPFullM + b, kCompute + 32);
+          if (lane == 0) trace_ev(tr, 3, n);
           named_bar_b(kBarDsFullM + b, kCompute + 32);
+          if (lane == 0) trace_ev(tr, 4, n);
           tc_fence_after();
 #pragma unroll
           for (int s = 0; s < 8; ++s)
@@ -640,8 +642,6 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     uint32_t uses = 0;           // bit g: parity of the fills of granule g so far
     int pq_g = 0, po_g = 0;      // granules of Q(P-1), dO(P-1)
     uint32_t pq_par = 0, po_par = 0;
-    int po2_g = 0;               // granule of dO(P-2) (merged d = 64 path, two buffer pairs)
-    uint32_t po2_par = 0;
     int P = 0;
     for (int j = 0;; ++j) {
       const int t = next_task_warp(j);
@@ -702,20 +702,19 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           for (int jj = 0; jj < 16; ++jj) pk[jj] = pack_bf16(pf[2 * jj], pf[2 * jj + 1]);
         }
         if (threadIdx.x == 0) trace_ev(tr, 6, P);
-        if (C::kMergeGK) {
-          // buffer pair pb was last read by the merged product of pair P-2 (which released
-          // the granules of Q / dO(P-2))
-          if (P >= 2) mbar_wait_sleep(&sm->g_empty[po2_g], po2_par);
-        } else if (P >= 1) {
-          mbar_wait_sleep(&sm->g_empty[po_g], po_par);  // dV(P-1) done: P buffer free
-        }
+        // P buffer free. Merged d = 64 path: buffer pair pb was last read by the merged
+        // product of pair P-2, which the issuer issued before S(P) -- s_full(P) (one commit
+        // tracking every earlier MMA) already implies it completed, no shared-memory poll.
+        if (!C::kMergeGK && P >= 1) mbar_wait_sleep(&sm->g_empty[po_g], po_par);  // dV(P-1) done
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           *reinterpret_cast<uint4*>(myP + sw128_offset(ql, (ch * 4 + c) * 16)) =
               make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         fence_proxy_async_smem();
         named_bar_arrive(C::kMergeGK ? kBarPFullM + b : kBarPFull, kCompute + 32);
+        if (threadIdx.x == 0) trace_ev(tr, 8, P);
         mbar_wait_sleep(&sm->dp_full[b], (P >> 1) & 1);
+        if (threadIdx.x == 0) trace_ev(tr, 9, P);
         tc_fence_after();
         {
           uint32_t rd[32];
@@ -736,6 +735,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           if (!C::kMergeGK) mbar_wait_sleep(&sm->g_empty[pq_g], pq_par);    // dK(P-1) done: dS buffer free
           if (ds_store) mbar_wait_sleep(&sm->ds_stored[pb], (use - 1) & 1);  // and its dS store read it
         }
+        if (threadIdx.x == 0) trace_ev(tr, 10, P);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           *reinterpret_cast<uint4*>(myS + sw128_offset(ql, (ch * 4 + c) * 16)) =
@@ -744,7 +744,6 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         named_bar_arrive(C::kMergeGK ? kBarDsFullM + b : kBarDsFull, kCompute + 32);
         if (ds_store) mbar_arrive(&sm->ds_full[pb]);  // for the dS store warp
         if (threadIdx.x == 0) trace_ev(tr, 7, P);
-        po2_g = po_g, po2_par = po_par;
         pq_g = cq_g, pq_par = cq_par, po_g = co_g, po_par = co_par;
       }
     }
