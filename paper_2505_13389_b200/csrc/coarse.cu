@@ -54,6 +54,10 @@ __device__ __forceinline__ float canon_expf(float x) { return __double2float_rn(
 
 // --------------------------------------------------------------------------- softmax + top-k
 // One warp per (b,h,row). Dynamic smem per warp: nc floats + 256-bin histogram.
+// kFast (the tcgen05 / bf16 coarse mode, whose scores are not the canonical fp32 ones
+// anyway): exp2 on MUFU, a warp-tree row sum and one reciprocal instead of the canonical
+// double-precision exp, the sequential lane-0 sum and per-element IEEE divisions.
+template <bool kFast>
 __global__ void __launch_bounds__(128) coarse_softmax_topk_kernel(int64_t rows, int nc, int k,
                                                                    float* __restrict__ ac, int32_t* __restrict__ sel,
                                                                    uint32_t* __restrict__ bitmap, int words,
@@ -75,6 +79,26 @@ __global__ void __launch_bounds__(128) coarse_softmax_topk_kernel(int64_t rows, 
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if constexpr (kFast) {
+    const float ml2 = m * 1.4426950408889634f;
+    float part = 0.f;
+    for (int j = lane; j < nc; j += 32) {
+      float e;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fmaf(fv[j], 1.4426950408889634f, -ml2)));
+      fv[j] = e;
+      part += e;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    const float inv = 1.0f / part;
+    for (int j = lane; j < nc; j += 32) {
+      const float p = fv[j] * inv;
+      fv[j] = p;
+      arow[j] = p;
+      if (pbf) pbf[row * nc + j] = __float2bfloat16_rn(p);
+    }
+    __syncwarp();
+  } else {
   // exact max as the oracle's sequential std::max (identical for non-NaN input)
   for (int j = lane; j < nc; j += 32) fv[j] = canon_expf(__fsub_rn(fv[j], m));
   __syncwarp();
@@ -97,6 +121,7 @@ __global__ void __launch_bounds__(128) coarse_softmax_topk_kernel(int64_t rows, 
     if (pbf) pbf[row * nc + j] = __float2bfloat16_rn(p);  // tcgen05 mode: the A operand of Oc = P Vc
   }
   __syncwarp();
+  }
 
   // radix select of the k-th largest bit pattern
   uint32_t prefix = 0, mask = 0;
@@ -368,11 +393,11 @@ int launch_coarse_forward(const vsa_layout_t& L, int64_t bh, int64_t d, const fl
     const int64_t rows = bh * nc;
     const size_t smem = 4 * (nc + 256) * sizeof(uint32_t);
     int rc0 = cuda_status(
-        cudaFuncSetAttribute(coarse_softmax_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+        cudaFuncSetAttribute(coarse_softmax_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
         "coarse_softmax_topk_kernel: shared memory");
     if (rc0) return rc0;
-    coarse_softmax_topk_kernel<<<unsigned((rows + 3) / 4), 128, smem, st>>>(rows, nc, int(top_k), ac, sel, bitmap,
-                                                                            words, nullptr);
+    coarse_softmax_topk_kernel<false><<<unsigned((rows + 3) / 4), 128, smem, st>>>(rows, nc, int(top_k), ac, sel,
+                                                                                   bitmap, words, nullptr);
     int rc = kernel_status("coarse_softmax_topk_kernel");
     if (rc) return rc;
   }
@@ -504,11 +529,11 @@ int launch_coarse_forward_bf16(const vsa_layout_t& L, int64_t bh, int64_t d, con
     const int64_t rows = bh * nc;
     const size_t smem = 4 * (nc + 256) * sizeof(uint32_t);
     rc = cuda_status(
-        cudaFuncSetAttribute(coarse_softmax_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+        cudaFuncSetAttribute(coarse_softmax_topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
         "coarse_softmax_topk_kernel: shared memory");
     if (rc) return rc;
-    coarse_softmax_topk_kernel<<<unsigned((rows + 3) / 4), 128, smem, st>>>(rows, nc, int(top_k), ac, sel, bitmap,
-                                                                            words, w.p);
+    coarse_softmax_topk_kernel<true><<<unsigned((rows + 3) / 4), 128, smem, st>>>(rows, nc, int(top_k), ac, sel,
+                                                                                  bitmap, words, w.p);
     rc = kernel_status("coarse_softmax_topk_kernel");
     if (rc) return rc;
   }
