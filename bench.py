@@ -394,7 +394,7 @@ def run_ours(args, rank, world, local_rank):
     # the binding resource of the fine kernels: the SM's shared-memory data pipe
     # (tensor-core operand reads + thread shared stores), from the committed ncu summary
     smem_pipe = None
-    npath = os.path.join(ROOT, "profiles", "ncu_r1d_kernels.json")
+    npath = os.path.join(ROOT, "profiles", "ncu_r2k_kernels.json")
     if os.path.exists(npath) and args.config == "wan13" and d == 128:
         try:
             with open(npath) as f:
@@ -462,7 +462,7 @@ def run_ours(args, rank, world, local_rank):
                      "smem_pipe_busy_pct": smem_pipe,
                      "note": "N=64 SS UMMAs are capped at 2/3 of the tensor peak by the 128 B/cycle SMEM "
                              "operand port; smem_pipe_busy_pct = ncu TC + LSU shared wavefronts per kernel "
-                             "(profiles/ncu_r1d_kernels.json, DESIGN.md section 4)"},
+                             "(profiles/ncu_r2k_kernels.json, DESIGN.md section 4)"},
         "l2_roofline": l2_roof,
         "stages": stages,
         "dense_baseline": dense,
