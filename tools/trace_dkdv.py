@@ -33,7 +33,7 @@ vsa.lib().vsa_debug_trace(None, 0, 0, 0)
 b = buf.cpu().tolist()
 ev = {(i // 256, i % 256): b[i] for i in range(cap) if b[i] != 0}
 t0 = min(ev.values())
-cols = [("gotS", 5), ("Prdy", 6), ("Pst", 8), ("gotdP", 9), ("dSfree", 10), ("done", 7), ("iP", 3), ("iDs", 4)]
+cols = [("preS", 11), ("gotS", 5), ("Prdy", 6), ("Pst", 8), ("gotdP", 9), ("dSfree", 10), ("done", 7), ("iP", 3), ("iDs", 4)]
 print("  p " + "".join(f"{n:>8s}" for n, _ in cols))
 for p in range(20, 60):
     row = [ev.get((code, p)) for _, code in cols]
