@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       mbar_init(&sm->acc_free[b], kEpiThreads);
     }
     for (int b = 0; b < NPB; ++b) {
-      mbar_init(&sm->ds_full[b], kCompute);
+      mbar_init(&sm->ds_full[b], kCompute / 32);  // one elected arrival per compute warp
       mbar_init(&sm->ds_stored[b], 1);
     }
     fence_barrier_init();
@@ -752,7 +752,10 @@ __global__ void __launch_bounds__(kKVThreads, 1)
               make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         fence_proxy_async_smem();
         named_bar_arrive(C::kMergeGK ? kBarDsFullM + b : kBarDsFull, kCompute + 32);
-        if (ds_store) mbar_arrive(&sm->ds_full[pb]);  // for the dS store warp
+        if (ds_store) {  // for the dS store warp: one arrival per warp (the stores of every lane
+          __syncwarp();  // and their proxy fences precede it), not 256 shared-memory atomics
+          if (lane == 0) mbar_arrive(&sm->ds_full[pb]);
+        }
         if (threadIdx.x == 0) trace_ev(tr, 7, P);
         pq_g = cq_g, pq_par = cq_par, po_g = co_g, po_par = co_par;
       }
