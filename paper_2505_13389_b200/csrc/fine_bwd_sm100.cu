@@ -52,6 +52,7 @@ constexpr int kEpiThreads = 128;
 // register budgets (setmaxnreg): compute / epilogue / producer-store-issuer-watcher warps
 constexpr int kKVRegCmp = 160, kKVRegEpi = 96, kKVRegCtl = 72;
 constexpr int kCompute = 256;  // two warpgroups
+constexpr int kCmpGroup = 128;  // merged d = 64 path: one warpgroup per pair (ping-pong by pair parity)
 
 __device__ __forceinline__ float ex2b(float x) {
   float y;
@@ -79,9 +80,9 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
 // waits for the P / dS buffers' release), sd_free alternates by pair parity, and the granule
 // rendezvous is a bar.sync on both sides (pairs up in order on one ID).
 constexpr int kBarPFull = 2, kBarDsFull = 3, kBarSdFree = 4 /* 4,5 */, kBarGran = 6;
-// merged d = 64 path (two {P, dS} buffer pairs: the compute warps may run one pair ahead
-// of the issuer's P / dS rendezvous): one barrier per pair parity
-constexpr int kBarPFullM = 7 /* 7,8 */, kBarDsFullM = 9 /* 9,10 */;
+// merged d = 64 path (two {P, dS} buffer pairs, one compute warpgroup per pair parity):
+// one P + dS rendezvous per pair parity
+constexpr int kBarDsFullM = 9 /* 9,10 */;
 
 __device__ __forceinline__ void tmem_ld32_raw(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       mbar_init(&sm->acc_free[b], kEpiThreads);
     }
     for (int b = 0; b < NPB; ++b) {
-      mbar_init(&sm->ds_full[b], kCompute / 32);  // one elected arrival per compute warp
+      mbar_init(&sm->ds_full[b], (C::kMergeGK ? kCmpGroup : kCompute) / 32);  // one arrival per compute warp
       mbar_init(&sm->ds_stored[b], 1);
     }
     fence_barrier_init();
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     // sel[qcube] — then release the buffer to the compute warps.
     if (lane == 0) {
       if (ds_store) tma_prefetch_desc(&tm_ds);
+      const uint64_t pol = l2_policy_evict_first();  // dS: written once, read once by dQ
       int P = 0;  // global pair index
       for (int j = 0;; ++j) {
         const int t = next_task(j, true);
@@ -357,10 +359,10 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           mbar_wait(&sm->ds_full[b], (P / NPB) & 1);
           const int e = T.beg + 2 * p;
           uint8_t* myS = sS + b * C::kPBStride;
-          tma_store_2d(&tm_ds, myS, 0, int((base + int64_t(T.list[e]) * k_sel + ds_pos[base + e]) * 64));
+          tma_store_2d_hint(&tm_ds, myS, 0, int((base + int64_t(T.list[e]) * k_sel + ds_pos[base + e]) * 64), pol);
           if (2 * p + 1 < T.nq)
-            tma_store_2d(&tm_ds, myS + 8192, 0,
-                         int((base + int64_t(T.list[e + 1]) * k_sel + ds_pos[base + e + 1]) * 64));
+            tma_store_2d_hint(&tm_ds, myS + 8192, 0,
+                              int((base + int64_t(T.list[e + 1]) * k_sel + ds_pos[base + e + 1]) * 64), pol);
           bulk_commit_group();
           bulk_wait_group_read0();
           mbar_arrive(&sm->ds_stored[b]);
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         }
         const int g = seq.next(i);
         mbar_wait_warp(&sm->g_full[g], (fills >> g) & 1);
+        if (lane == 0) trace_ev(tr, 3, i);
         fills ^= 1u << g;
         named_bar_b(kBarGran, 64);  // rendezvous with the issuer, in consumption order
       }
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       const int g0 = seq.next(2 * n);
       if (b) gq1 = g0; else gq0 = g0;
       const uint64_t q0 = dG0 + uint64_t((g0 * C::kGran) >> 4);
-      if (n >= 2) named_bar_b(kBarSdFree + b, kCompute + 32);
+      if (n >= 2) named_bar_b(kBarSdFree + b, (C::kMergeGK ? kCmpGroup : kCompute) + 32);
       named_bar_b(kBarGran, 64);
       tc_fence_after();
 #pragma unroll
@@ -513,9 +516,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           const int go = b ? go1 : go0, gq = b ? gq1 : gq0;  // dO(n) in 2m, Q(n) in 2m + 1
           const uint64_t da = make_sdesc_sw128(aG + uint32_t(go * C::kGran), uint32_t(C::kGran), 1024);
           if (p == 0 && acn >= 2) mbar_wait_warp(&sm->acc_free[ab], ((acn >> 1) & 1) ^ 1);
-          named_bar_b(kBarPFullM + b, kCompute + 32);
-          if (lane == 0) trace_ev(tr, 3, n);
-          named_bar_b(kBarDsFullM + b, kCompute + 32);
+          named_bar_b(kBarDsFullM + b, kCmpGroup + 32);  // P(n) and dS(n) written (group n & 1)
           if (lane == 0) trace_ev(tr, 4, n);
           tc_fence_after();
 #pragma unroll
@@ -571,7 +572,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       ++acn;
     }
     // consume the compute warps' last S-buffer releases (no later S waits on them)
-    for (int n = P >= 2 ? P - 2 : 0; n < P; ++n) named_bar_b(kBarSdFree + (n & 1), kCompute + 32);
+    for (int n = P >= 2 ? P - 2 : 0; n < P; ++n)
+      named_bar_b(kBarSdFree + (n & 1), (C::kMergeGK ? kCmpGroup : kCompute) + 32);
   } else if (warp >= 12) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kKVRegEpi));
     // ---------------------------------------------------------------- epilogue warps
@@ -627,6 +629,100 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         mbar_arrive(&sm->acc_free[ab]);
         ++acn;
       }
+    }
+  } else if (warp < 8 && C::kMergeGK) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kKVRegCmp));
+    // d = 64 (merged dV / dK product): the two compute warpgroups ping-pong over pairs --
+    // warpgroup g takes the pairs with P & 1 == g (its S / dP TMEM buffers and {P, dS}
+    // buffer pair are the parity-g ones), each warp its 32 query rows x all 64 key columns.
+    // One group's exponentials (MUFU) overlap the other group's dS math, stores and waits;
+    // with all eight warps on every pair the per-pair chain (exps, then the dS / store /
+    // poll tail) ran serially at ~1500 cycles per pair (profiles/trace_dkdv_d64_r2.txt).
+    // S and dP of a pair are both read before any store: P and dS are produced together in
+    // two 32-column halves (P never round-trips), and the merged product needs both anyway.
+    const int g = warp >> 2;
+    const int ql = (warp & 3) * 32 + lane;  // query lane within the pair
+    const uint32_t lrow = tbase + (uint32_t((warp & 3) * 32) << 16);
+    int P = 0;
+    for (int j = 0;; ++j) {
+      const int t = next_task_warp(j);
+      if (t < 0) break;
+      const Task T = task(t);
+      auto qcube_of = [&](int pp) -> int {
+        return (pp < T.npairs && (ql < 64 || 2 * pp + 1 < T.nq)) ? T.list[T.beg + 2 * pp + (ql >> 6)] : -1;
+      };
+      auto row_stats = [&](int qcube, float& l2, float& dlt) {
+        l2 = 0.f;
+        dlt = 0.f;
+        if (qcube >= 0) {
+          const int64_t trow = int64_t(T.row0) + int64_t(qcube) * 64 + (ql & 63);
+          l2 = lse[trow];
+          dlt = delta[trow];
+        }
+      };
+      const int p0 = (g - P) & 1;  // this group's first pair of the task
+      float nl2, ndl;
+      row_stats(qcube_of(p0), nl2, ndl);
+      int nqc = qcube_of(p0 + 2);
+      const uint64_t kmask = L.mask ? cube_token_mask(L, T.kc) : ~uint64_t(0);
+      for (int p = p0; p < T.npairs; p += 2) {
+        const int n = P + p, b = g, use = n >> 1;
+        uint8_t* myP = sP + b * C::kPBStride;
+        uint8_t* myS = sS + b * C::kPBStride;
+        const bool valid = ql < 64 || (2 * p + 1 < T.nq);  // warp-uniform
+        const float lse2 = nl2 * 1.4426950408889634f, dl = ndl;
+        row_stats(nqc, nl2, ndl);  // pair p + 2
+        nqc = qcube_of(p + 4);
+        // the {P, dS} buffer pair b was last read by the merged product of pair n - 2,
+        // issued before S(n): s_full(n) implies it completed; the dS store of pair n - 2
+        // must have read its dS (ds_stored)
+        if (ds_store && use >= 1) mbar_wait_sleep(&sm->ds_stored[b], (use - 1) & 1);
+        mbar_wait_sleep(&sm->s_full[b], use & 1);
+        if (threadIdx.x == 0 || threadIdx.x == 128) trace_ev(tr, 5, n);
+        mbar_wait_sleep(&sm->dp_full[b], use & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t rs[32], rd[32];
+          tmem_ld32_raw(lrow + b * 64 + h * 32, rs);
+          tmem_ld32_raw(lrow + 128 + b * 64 + h * 32, rd);
+          tmem_wait_ld();
+          const uint32_t km = uint32_t(kmask >> (32 * h));
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t pkp[4], pkd[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int e = 8 * c + 2 * i;
+              float a0, a1;
+              f2_unpack(ffma2(f2(__uint_as_float(rs[e]), __uint_as_float(rs[e + 1])), f2(scale_log2, scale_log2),
+                              f2(-lse2, -lse2)),
+                        a0, a1);
+              float p0v = valid ? ex2b(a0) : 0.f, p1v = valid ? ex2b(a1) : 0.f;
+              if (!((km >> e) & 1u)) p0v = 0.f;  // mask pad: P = 0 on padded keys (dS follows)
+              if (!((km >> (e + 1)) & 1u)) p1v = 0.f;
+              float d0, d1;
+              f2_unpack(fmul2(f2(p0v, p1v), fadd2(f2(__uint_as_float(rd[e]), __uint_as_float(rd[e + 1])), f2(-dl, -dl))),
+                        d0, d1);
+              pkp[i] = pack_bf16(p0v, p1v);
+              pkd[i] = pack_bf16(d0, d1);
+            }
+            const uint32_t off = sw128_offset(ql, (4 * h + c) * 16);
+            *reinterpret_cast<uint4*>(myP + off) = make_uint4(pkp[0], pkp[1], pkp[2], pkp[3]);
+            *reinterpret_cast<uint4*>(myS + off) = make_uint4(pkd[0], pkd[1], pkd[2], pkd[3]);
+          }
+        }
+        tc_fence_before();
+        named_bar_arrive(kBarSdFree + b, kCmpGroup + 32);  // S / dP buffers b read
+        fence_proxy_async_smem();
+        named_bar_arrive(kBarDsFullM + b, kCmpGroup + 32);
+        if (ds_store) {  // for the dS store warp: one arrival per warp
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm->ds_full[b]);
+        }
+        if (threadIdx.x == 0 || threadIdx.x == 128) trace_ev(tr, 7, n);
+      }
+      P += T.npairs;
     }
   } else if (warp < 8) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kKVRegCmp));
@@ -721,7 +817,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           *reinterpret_cast<uint4*>(myP + sw128_offset(ql, (ch * 4 + c) * 16)) =
               make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         fence_proxy_async_smem();
-        named_bar_arrive(C::kMergeGK ? kBarPFullM + b : kBarPFull, kCompute + 32);
+        named_bar_arrive(kBarPFull, kCompute + 32);
         if (threadIdx.x == 0) trace_ev(tr, 8, P);
         mbar_wait_sleep(&sm->dp_full[b], (P >> 1) & 1);
         if (threadIdx.x == 0) trace_ev(tr, 9, P);
@@ -751,7 +847,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           *reinterpret_cast<uint4*>(myS + sw128_offset(ql, (ch * 4 + c) * 16)) =
               make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         fence_proxy_async_smem();
-        named_bar_arrive(C::kMergeGK ? kBarDsFullM + b : kBarDsFull, kCompute + 32);
+        named_bar_arrive(kBarDsFull, kCompute + 32);
         if (ds_store) {  // for the dS store warp: one arrival per warp (the stores of every lane
           __syncwarp();  // and their proxy fences precede it), not 256 shared-memory atomics
           if (lane == 0) mbar_arrive(&sm->ds_full[pb]);
@@ -838,6 +934,7 @@ __global__ void __launch_bounds__(kDQThreads, 2)
     if (lane == 0) {
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_ds);
+      const uint64_t pol = l2_policy_evict_first();  // dS tiles: read once (keep the K tiles in L2)
       // The dS stream comes from HBM (the K pairs hit L2): keep kDQPrefetch tiles in
       // flight into L2 ahead of the 2-stage SMEM ring (measured: ~0.05 ms per step).
       const int pf0 = min(kDQPrefetch, k_sel);
@@ -855,12 +952,12 @@ __global__ void __launch_bounds__(kDQThreads, 2)
         const int ka = srow[2 * p];
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_2d(sK + c * C::kPairChunk, &tm_k, &sm->full[st], c * 64, row0 + ka * 64);
-        tma_load_2d(sD, &tm_ds, &sm->full[st], 0, int(ds_row0 + int64_t(2 * p) * 64));
+        tma_load_2d_hint(sD, &tm_ds, &sm->full[st], 0, int(ds_row0 + int64_t(2 * p) * 64), pol);
         if (hb) {
           const int kb = srow[2 * p + 1];
           for (int c = 0; c < C::kChunks; ++c)
             tma_load_2d(sK + c * C::kPairChunk + 8192, &tm_k, &sm->full[st], c * 64, row0 + kb * 64);
-          tma_load_2d(sD + 8192, &tm_ds, &sm->full[st], 0, int(ds_row0 + int64_t(2 * p + 1) * 64));
+          tma_load_2d_hint(sD + 8192, &tm_ds, &sm->full[st], 0, int(ds_row0 + int64_t(2 * p + 1) * 64), pol);
         }
       }
     }

@@ -2,9 +2,9 @@
 """Debug: per-pair event trace of one dK/dV CTA (current kernel's probes). Needs a
 -DVSA_TRACE build (tools/build_variant.sh trace fine_bwd_sm100.cu -DVSA_TRACE, then
 VSA_LIB_PATH=.../libvsa_trace.so). usage: trace_dkdv.py [wan13|dit]
-Columns (cycles from the first event): compute warps got S, P ready, P stored (PFull),
-got dP, dS buffer free, done (DsFull); issuer past PFull / past DsFull of the merged
-d = 64 product."""
+Columns (cycles from the first event): producer issued the Q / dO granule of the pair,
+the watcher saw it land, the compute warps got S (and dP), finished P / dS, and the
+issuer passed the P / dS rendezvous of the merged d = 64 product."""
 import ctypes as C
 import sys
 
@@ -33,8 +33,8 @@ vsa.lib().vsa_debug_trace(None, 0, 0, 0)
 b = buf.cpu().tolist()
 ev = {(i // 256, i % 256): b[i] for i in range(cap) if b[i] != 0}
 t0 = min(ev.values())
-cols = [("preS", 11), ("gotS", 5), ("Prdy", 6), ("Pst", 8), ("gotdP", 9), ("dSfree", 10), ("done", 7), ("iP", 3), ("iDs", 4)]
-print("  p " + "".join(f"{n:>8s}" for n, _ in cols))
+cols = [("ldQ", 2, 0), ("ldO", 2, 1), ("inQ", 3, 0), ("inO", 3, 1), ("gotS", 5, None), ("done", 7, None), ("iG", 4, None)]
+print("  p " + "".join(f"{n:>8s}" for n, _, _ in cols))
 for p in range(20, 60):
-    row = [ev.get((code, p)) for _, code in cols]
+    row = [ev.get((code, 2 * p + k if k is not None else p)) for _, code, k in cols]
     print(f"{p:3d} " + "".join(f"{(r - t0) if r else -1:8d}" for r in row))
