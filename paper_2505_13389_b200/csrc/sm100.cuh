@@ -183,7 +183,11 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 // dO / K tiles the fine kernels re-read from L2 many times.
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t p;
+#ifdef VSA_L2_HINT_NORMAL  // A/B: the same hinted instructions with the default (evict_normal) policy
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+#else
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#endif
   return p;
 }
 __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1,

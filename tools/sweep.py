@@ -10,7 +10,8 @@ Per point: fine forward and fine backward device times from the operator's nativ
 stage events (fine_fwd = K4+K5, fine_bwd = K6b+K6c), the whole-operator forward
 (K1..K5) and backward (K6a..K6d) times, effective TFLOP/s on the algorithmic FLOPs
 (fine fwd 4*64^2*d, bwd 10*64^2*d per selected tile) and the speed-up over dense.
-Inputs: torch.randn bf16, larger than L2 at 32^3."""
+Inputs: torch.randn bf16, larger than L2 at 32^3. Each point: 3 warm-up steps, then the
+best of three rounds of --reps steps, after a ~2 s warm-up of the GPU."""
 import argparse
 import json
 import os
@@ -35,18 +36,22 @@ def measure(L, H, d, k, xs, reps):
     for _ in range(3):
         step()
     torch.cuda.synchronize()
-    op.timing(True)
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    e[0].record()
-    for _ in range(reps):
-        step()
-    e[1].record()
-    st = op.stage_ms()
-    op.timing(False)
-    torch.cuda.synchronize()
-    step_ms = e[0].elapsed_time(e[1]) / reps
+    best = None
+    for _ in range(3):  # best of three rounds (short launches on a shared box are noisy)
+        op.timing(True)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e[0].record()
+        for _ in range(reps):
+            step()
+        e[1].record()
+        st = op.stage_ms()
+        op.timing(False)
+        torch.cuda.synchronize()
+        step_ms = e[0].elapsed_time(e[1]) / reps
+        if best is None or step_ms < best[0]:
+            best = (step_ms, st)
     del op
-    return step_ms, st
+    return best
 
 
 def main():
@@ -59,6 +64,13 @@ def main():
     H = 16
     rows = []
     t0 = time.time()
+    # warm the GPU to its steady clocks before the first point (~2 s of dense work)
+    Lw = vsa.TileLayout(32, 32, 32)
+    xw = [torch.randn((1, H, Lw.seq_len, 128), device="cuda").bfloat16() for _ in range(6)]
+    tw = time.time()
+    while time.time() - tw < 2.0:
+        measure(Lw, H, 128, Lw.num_cubes, xw, 1)
+    del xw
     for n in (int(x) for x in args.grids.split(",")):
         L = vsa.TileLayout(n, n, n)
         nc = L.num_cubes
