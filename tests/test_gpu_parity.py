@@ -221,14 +221,15 @@ def test_host_pipeline_matches_resident_op(vsa):
     ins = [to_dev(x, dt) for x in (p.q, p.k, p.v, p.gc, p.gf, p.dout)]
     op = vsa.VsaOp(L, p.B, p.H, p.d, p.top_k, dtype=dt)
     ref = [op.forward(*ins[:5]).clone()] + [t.clone() for t in op.backward(ins[5])]
-    for chunks in (1, 4, 6):
-        pipe = vsa.VsaHostPipeline(L, p.B, p.H, p.d, p.top_k, chunks=chunks, dtype=dt)
+    for chunks, slots in ((1, 2), (4, 2), (6, 3), (6, 4), (5, 3)):  # ragged groups at 5 chunks of 6 units
+        pipe = vsa.VsaHostPipeline(L, p.B, p.H, p.d, p.top_k, chunks=chunks, dtype=dt, slots=slots)
         hin = [t.cpu().pin_memory() for t in ins]
         hout = [torch.empty(t.shape, dtype=dt, pin_memory=True) for t in ref]
-        pipe.run(hin, hout)
+        for _ in range(2):  # the second run reuses every slot's buffers and events
+            pipe.run(hin, hout)
         torch.cuda.synchronize()
         for a, b in zip(hout, ref):
-            assert torch.equal(a, b.cpu()), f"chunks={chunks}"
+            assert torch.equal(a, b.cpu()), f"chunks={chunks} slots={slots}"
 
 
 @pytest.mark.parametrize("d", [128, 64])
