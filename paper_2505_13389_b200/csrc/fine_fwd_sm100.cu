@@ -46,6 +46,7 @@
 // TMEM columns: S^T [0,64) [64,128) by gp parity, O^T [128,192) [192,256) by cube
 // parity. Row-sum partials (per key lane) stay in registers.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -646,6 +647,15 @@ int launch_fine_forward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, cons
   if (d == 128)
     return fwd_launch<128>(L, bh, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube, flags, out, task_begin,
                            task_end, st);
+  // d = 64: the ping-pong kernel (two softmax groups, fine_fwd_pp_sm100.cu); VSA_FWD_PP=0
+  // selects this file's single-group kernel (A/B measurements)
+  static const bool pp = [] {
+    const char* e = std::getenv("VSA_FWD_PP");
+    return e == nullptr || e[0] != '0';
+  }();
+  if (pp)
+    return launch_fine_forward_pp_sm100(L, bh, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube, flags,
+                                        out, task_begin, task_end, st);
   return fwd_launch<64>(L, bh, q, k, v, sel, top_k, o_fine, lse, row_max, gc, gf, oc_cube, flags, out, task_begin,
                         task_end, st);
 }

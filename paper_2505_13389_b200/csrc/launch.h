@@ -88,6 +88,11 @@ int launch_fine_backward_simt(const vsa_layout_t& L, int64_t bh, int64_t d, int3
 // tcgen05 kernels (bf16, cube = 64, d in {64, 128}); return 1 if the shape is unsupported
 bool sm100_fine_supported(const vsa_layout_t& L, int64_t d, int32_t dtype);
 bool sm100_fine_bwd_supported(const vsa_layout_t& L, int64_t d, int32_t dtype);
+// d = 64 forward with two softmax groups in ping-pong (fine_fwd_pp_sm100.cu)
+int launch_fine_forward_pp_sm100(const vsa_layout_t& L, int64_t bh, const void* q, const void* k, const void* v,
+                                 const int32_t* sel, int64_t top_k, void* o_fine, float* lse, float* row_max,
+                                 const void* gc, const void* gf, const float* oc_cube, int32_t flags, void* out,
+                                 int64_t task_begin, int64_t task_end, cudaStream_t st);
 int launch_fine_forward_sm100(const vsa_layout_t& L, int64_t bh, int64_t d, const void* q, const void* k,
                               const void* v, const int32_t* sel, int64_t top_k, void* o_fine, float* lse,
                               float* row_max, const void* gc, const void* gf, const float* oc_cube, int32_t flags,

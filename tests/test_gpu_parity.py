@@ -114,7 +114,12 @@ def test_fine_forward_backward(vsa, cfg, dtype):
     dsel = to_dev(sel, torch.int32)
     res = vsa.fine_forward(L, dq_, dk_, dv_, dsel)
     assert_close(host(res.out), fo, dtype, "fine out")
-    np.testing.assert_allclose(res.row_lse.cpu().numpy().reshape(flse.shape), flse, atol=2e-3 if dtype != torch.float32 else 1e-4)
+    # bf16: P is rounded to bf16 for the P.V product; at d = 64 the forward sums the
+    # softmax denominator on the tensor core over the same bf16 P (row 64 of O^T,
+    # fine_fwd_pp_sm100.cu), so lse carries that rounding (<= 2^-9 relative in l, a few
+    # 1e-3 in log l where a few keys dominate a row); O itself is normalised consistently
+    np.testing.assert_allclose(res.row_lse.cpu().numpy().reshape(flse.shape), flse,
+                               atol=5e-3 if dtype != torch.float32 else 1e-4)
     g = vsa.fine_backward(L, dq_, dk_, dv_, dsel, do_, res.row_lse, out=res.out)
     for got, ref, n in zip(g, (fdq, fdk, fdv), ("dq", "dk", "dv")):
         assert_close(host(got), ref, dtype, n)
