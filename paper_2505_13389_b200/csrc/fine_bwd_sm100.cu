@@ -153,7 +153,8 @@ __device__ __forceinline__ void write_rows(const DevLayout& L, int64_t u, int cu
 //   dV(p) += dOpair^T . P -> frees dO(p), P buffer   (needs P(p) from the compute warps)
 //   dK(p) += Qpair^T . dS -> frees Q(p),  dS buffer  (needs dS(p))
 // The compute warps write P(p) as soon as S(p) is in, before dP(p) is read, so
-// dV(p) overlaps the dS math.
+// dV(p) overlaps the dS math. (d = 64: one merged dV / dK product per pair, issue order
+// S(p+1), dP(p+1), G(p), and the two compute warpgroups alternate pairs -- KVCfg below.)
 // Granule of streamed item i (item 2p = Q(p), 2p+1 = dO(p)). Granules are handed
 // out in the order they are released: the first NG items take granules 0..NG-1,
 // then item NG+j takes the granule of the j-th release. The tensor pipe releases
