@@ -475,8 +475,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       tc_fence_after();
 #pragma unroll
       for (int s = 0; s < D / 16; ++s)
-        umma_bf16_warp(tbase + b * 64, q0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
-                       dK0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+        umma_bf16_warp_off(tbase + b * 64, q0, uint32_t(((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
+                           dK0, uint32_t(((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
       umma_commit_warp(&sm->s_full[b]);
     };
     auto issue_dp = [&](int n) {
@@ -488,8 +488,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       tc_fence_after();
 #pragma unroll
       for (int s = 0; s < D / 16; ++s)
-        umma_bf16_warp(tbase + 128 + b * 64, o0 + (((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
-                       dV0 + (((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+        umma_bf16_warp_off(tbase + 128 + b * 64, o0, uint32_t(((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
+                           dV0, uint32_t(((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
       umma_commit_warp(&sm->dp_full[b]);
     };
     for (int j = 0;; ++j) {
@@ -520,10 +520,10 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           named_bar_b(kBarDsFullM + b, kCmpGroup + 32);  // P(n) and dS(n) written (group n & 1)
           if (lane == 0) trace_ev(tr, 4, n);
           tc_fence_after();
+          const uint64_t db = dPS0 + uint64_t(((n % NPB) * C::kPBStride) >> 4);
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_bf16_warp(tV, da + uint64_t(s * 128), dPS0 + uint64_t(((n % NPB) * C::kPBStride) >> 4) + uint64_t(s * 128),
-                           idGK, (p > 0 || s > 0) ? 1u : 0u);
+            umma_bf16_warp_off(tV, da, uint32_t(s * 128), db, uint32_t(s * 128), idGK, (p > 0 || s > 0) ? 1u : 0u);
           umma_commit_warp(&sm->g_empty[go]);
           umma_commit_warp(&sm->g_empty[gq]);
         }
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             tc_fence_after();
 #pragma unroll
             for (int s = 0; s < 8; ++s)
-              umma_bf16_warp(tV, da + uint64_t(s * 128), dP0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+              umma_bf16_warp_off(tV, da, uint32_t(s * 128), dP0, uint32_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
             umma_commit_warp(&sm->g_empty[g]);
           }
           if (p + 1 < npairs) {
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             tc_fence_after();
 #pragma unroll
             for (int s = 0; s < 8; ++s)
-              umma_bf16_warp(tK, da + uint64_t(s * 128), dS0 + uint64_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+              umma_bf16_warp_off(tK, da, uint32_t(s * 128), dS0, uint32_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
             umma_commit_warp(&sm->g_empty[g]);
           }
         }
@@ -977,12 +977,12 @@ __global__ void __launch_bounds__(kDQThreads, 2)
         if (hb) {
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_bf16_warp(tbase, ad + uint64_t(s * 128), bd + uint64_t(((s >> 2) * 8192 + (s & 3) * 32) >> 4), idG,
-                           (p > 0 || s > 0) ? 1u : 0u);
+            umma_bf16_warp_off(tbase, ad, uint32_t(s * 128), bd, uint32_t(((s >> 2) * 8192 + (s & 3) * 32) >> 4), idG,
+                               (p > 0 || s > 0) ? 1u : 0u);
         } else {  // a single-cube last pair contributes 64 keys
 #pragma unroll
           for (int s = 0; s < 4; ++s)
-            umma_bf16_warp(tbase, ad + uint64_t(s * 128), bd + uint64_t((s * 32) >> 4), idG, (p > 0 || s > 0) ? 1u : 0u);
+            umma_bf16_warp_off(tbase, ad, uint32_t(s * 128), bd, uint32_t((s * 32) >> 4), idG, (p > 0 || s > 0) ? 1u : 0u);
         }
         umma_commit_warp(&sm->empty[st]);
       }

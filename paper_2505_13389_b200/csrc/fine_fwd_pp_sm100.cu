@@ -375,38 +375,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (h == 0) bar_sync(kBGran, 64);  // both granules of the slot landed (load watcher)
         if (e == 0) {
           const int g = sc.sg, jj = sc.sjj, p = sc.sp, b = sc.nS() & 1, qb = jj & 1;
+          if (lane == 0) trace_ev(tr, 5, sc.sIdx);
           if (p == 0) mbar_wait_warp(&sm->q_full[g][qb], (jj >> 1) & 1);
           tc_fence_after();
           const uint64_t a0 = dG0 + uint64_t(goff >> 4), b0 = dQ0 + uint64_t(((g * 2 + qb) * kQBytes) >> 4);
-#pragma unroll
-          for (int s = 0; s < D / 16; ++s)
-            umma_bf16_warp(tbase + g * 128 + b * 64, a0 + uint64_t(s * 2), b0 + uint64_t(s * 2), idS, s > 0);
-          if (lane == 0) trace_ev(tr, 3, sc.sIdx);
+          umma_bf16_run<D / 16, 2, 2>(tbase + g * 128 + b * 64, a0, b0, idS, false);
           umma_commit_warp(&sm->s_full[g][b]);
           if (p == np - 1) umma_commit_warp(&sm->q_empty[g][qb]);
+          if (lane == 0) trace_ev(tr, 3, sc.sIdx);
           sc.adv_s();
         } else {
           const int g = sc.og, jj = sc.ojj, p = sc.op, b = sc.pw() & 1, tb = jj & 1;
+          if (lane == 0) trace_ev(tr, 15, sc.oIdx);
           bar_sync(kBPFull + 2 * g + b, 160);  // P^T(g, n) written
           if (p == 0 && jj >= 2) bar_sync(kBOFree + 2 * g + tb, 160);  // O^T(g, tb) read by the epilogue
           if (lane == 0) trace_ev(tr, 4, sc.oIdx);
           tc_fence_after();
           // A = [V^T ; ones ; 0]: MN-major, the second 64-row block at LBO, re-aimed at
-          // the 2 KB constant tile for every 16-key step
+          // the 2 KB constant tile for every 16-key step (start address +2048 B, LBO -2048 B:
+          // +128 / -128 in the descriptor's 16-byte units; the constant tile follows the ring)
           const uint32_t av = aG + goff;
           const uint64_t b0 = dP0 + uint64_t(((g * 2 + b) * 16384) >> 4);
-#pragma unroll
-          for (int s = 0; s < 8; ++s) {
-            const uint32_t as = av + uint32_t(s * 2048);
-            umma_bf16_warp(tbase + 256 + g * 128 + tb * 64, make_sdesc_sw128(as, aZ - as, 1024),
-                           b0 + uint64_t(s * 128), idO, (p > 0 || s > 0) ? 1u : 0u);
-          }
+          umma_bf16_run<8, 128u - (128u << 16), 128>(tbase + 256 + g * 128 + tb * 64,
+                                                      make_sdesc_sw128(av, aZ - av, 1024), b0, idO, p > 0);
           umma_commit_warp(&sm->o_done[g]);
           if (p == np - 1) umma_commit_warp(&sm->o_full[g][tb]);
+          if (h == 1) umma_commit_warp(&sm->g_empty[ring]);  // the slot's second MMA group
+          if (lane == 0) trace_ev(tr, 6, sc.oIdx);
           sc.adv_o();
         }
         if (h == 1) {  // the slot's second MMA group issued: free it when both complete
-          umma_commit_warp(&sm->g_empty[ring]);
+          if (e == 0) umma_commit_warp(&sm->g_empty[ring]);  // (an O event committed it above)
           if (++ring == kNS) ring = 0;
         }
         h ^= 1;

@@ -298,8 +298,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc_fence_after();
 #pragma unroll
         for (int s = 0; s < D / 16; ++s)
-          umma_bf16_warp(tbase + (gp & 1) * 64, a0 + (((s >> 2) * C::kChunkStride + (s & 3) * 32) >> 4),
-                         b0 + (((s >> 2) * 8192 + (s & 3) * 32) >> 4), idS, s > 0);
+          umma_bf16_warp_off(tbase + (gp & 1) * 64, a0, uint32_t(((s >> 2) * C::kChunkStride + (s & 3) * 32) >> 4),
+                             b0, uint32_t(((s >> 2) * 8192 + (s & 3) * 32) >> 4), idS, s > 0);
         umma_commit_warp(&sm->g_empty[g]);
         umma_commit_warp(&sm->s_full[gp & 1]);
         if (p == np - 1) umma_commit_warp(&sm->q_empty[qb]);
@@ -325,8 +325,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc_fence_after();
 #pragma unroll
         for (int s = 0; s < 8; ++s)
-          umma_bf16_warp(tbase + 128 + tb * 64, a0 + uint64_t(s * 128), b0 + uint64_t(s * 128), idO,
-                         (p > 0 || s > 0) ? 1u : 0u);
+          umma_bf16_warp_off(tbase + 128 + tb * 64, a0, uint32_t(s * 128), b0, uint32_t(s * 128), idO,
+                             (p > 0 || s > 0) ? 1u : 0u);
         umma_commit_warp(&sm->g_empty[g]);
         umma_commit_warp(&sm->o_done[gp & 1]);
         if (p == np - 1) umma_commit_warp(&sm->o_full[tb]);

@@ -267,6 +267,63 @@ __device__ __forceinline__ void umma_bf16_warp(uint32_t d_tmem, uint64_t adesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// umma_bf16_warp with the descriptors' offsets (16-byte units, start address / LBO fields)
+// added to their LOW words only: the fields never carry into the high word, which stays a
+// constant (SBO, version, swizzle) the compiler materialises without a 64-bit add. The MMA
+// warp shares its SM sub-partition with busy softmax / compute warps, so its instruction
+// count per MMA is a cost: ~9 instructions with 64-bit descriptor arithmetic, ~4 here.
+// (One elect for a whole run, the MMAs issued from a divergent branch, was 30 % slower in
+// the d = 64 forward than this warp-converged form: the elect stays inside the asm.)
+__device__ __forceinline__ void umma_bf16_warp_off(uint32_t d_tmem, uint64_t adesc, uint32_t aoff, uint64_t bdesc,
+                                                   uint32_t boff, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "mov.b64 a, {%1, %2};\n\t"
+      "mov.b64 b, {%3, %4};\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, p;\n\t}" ::"r"(d_tmem),
+      "r"(uint32_t(adesc) + aoff), "r"(uint32_t(adesc >> 32)), "r"(uint32_t(bdesc) + boff),
+      "r"(uint32_t(bdesc >> 32)), "r"(accumulate), "r"(idesc)
+      : "memory");
+}
+// A run of N (4 or 8) such MMAs whose offsets advance by compile-time steps, behind ONE
+// elect inside one asm block (warp-converged, predicated issue): the per-MMA elect / vote
+// and the re-materialised instruction descriptor of umma_bf16_warp_off go away.
+#define VSA_UMMA_NEXT                  \
+  "add.u32 al, al, %7;\n\t"            \
+  "add.u32 bl, bl, %8;\n\t"            \
+  "mov.b64 a, {al, %2};\n\t"           \
+  "mov.b64 b, {bl, %4};\n\t"           \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, 1;\n\t"
+#define VSA_UMMA_HEAD                  \
+  "{\n\t.reg .pred p, e;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t" \
+  "setp.ne.b32 p, %5, 0;\n\t"          \
+  "elect.sync _|e, 0xffffffff;\n\t"    \
+  "mov.b32 al, %1;\n\t"                \
+  "mov.b32 bl, %3;\n\t"                \
+  "mov.b64 a, {al, %2};\n\t"           \
+  "mov.b64 b, {bl, %4};\n\t"           \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, p;\n\t"
+template <int N, uint32_t kAStep, uint32_t kBStep>
+__device__ __forceinline__ void umma_bf16_run(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              bool acc_first) {
+  static_assert(N == 4 || N == 8, "umma_bf16_run: N = 4 or 8");
+  if constexpr (N == 4)
+    asm volatile(VSA_UMMA_HEAD VSA_UMMA_NEXT VSA_UMMA_NEXT VSA_UMMA_NEXT "}" ::"r"(d_tmem), "r"(uint32_t(adesc)),
+                 "r"(uint32_t(adesc >> 32)), "r"(uint32_t(bdesc)), "r"(uint32_t(bdesc >> 32)),
+                 "r"(acc_first ? 1u : 0u), "r"(idesc), "n"(kAStep), "n"(kBStep)
+                 : "memory");
+  else
+    asm volatile(VSA_UMMA_HEAD VSA_UMMA_NEXT VSA_UMMA_NEXT VSA_UMMA_NEXT VSA_UMMA_NEXT VSA_UMMA_NEXT VSA_UMMA_NEXT
+                     VSA_UMMA_NEXT "}" ::"r"(d_tmem),
+                 "r"(uint32_t(adesc)), "r"(uint32_t(adesc >> 32)), "r"(uint32_t(bdesc)), "r"(uint32_t(bdesc >> 32)),
+                 "r"(acc_first ? 1u : 0u), "r"(idesc), "n"(kAStep), "n"(kBStep)
+                 : "memory");
+}
+#undef VSA_UMMA_HEAD
+#undef VSA_UMMA_NEXT
+
 __device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
