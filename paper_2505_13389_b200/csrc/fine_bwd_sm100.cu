@@ -473,10 +473,14 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       if (n >= 2) named_bar_b(kBarSdFree + b, (C::kMergeGK ? kCmpGroup : kCompute) + 32);
       named_bar_b(kBarGran, 64);
       tc_fence_after();
+      if constexpr (D == 64) {
+        umma_bf16_run<4, 2, 2>(tbase + b * 64, q0, dK0, idSD, false);
+      } else {
 #pragma unroll
-      for (int s = 0; s < D / 16; ++s)
-        umma_bf16_warp_off(tbase + b * 64, q0, uint32_t(((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
-                           dK0, uint32_t(((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+        for (int s = 0; s < D / 16; ++s)
+          umma_bf16_warp_off(tbase + b * 64, q0, uint32_t(((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
+                             dK0, uint32_t(((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+      }
       umma_commit_warp(&sm->s_full[b]);
     };
     auto issue_dp = [&](int n) {
@@ -486,10 +490,14 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       const uint64_t o0 = dG0 + uint64_t((g1 * C::kGran) >> 4);
       named_bar_b(kBarGran, 64);
       tc_fence_after();
+      if constexpr (D == 64) {
+        umma_bf16_run<4, 2, 2>(tbase + 128 + b * 64, o0, dV0, idSD, false);
+      } else {
 #pragma unroll
-      for (int s = 0; s < D / 16; ++s)
-        umma_bf16_warp_off(tbase + 128 + b * 64, o0, uint32_t(((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
-                           dV0, uint32_t(((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+        for (int s = 0; s < D / 16; ++s)
+          umma_bf16_warp_off(tbase + 128 + b * 64, o0, uint32_t(((s >> 2) * C::kPairChunk + (s & 3) * 32) >> 4),
+                             dV0, uint32_t(((s >> 2) * C::kCubeChunk + (s & 3) * 32) >> 4), idSD, s > 0);
+      }
       umma_commit_warp(&sm->dp_full[b]);
     };
     for (int j = 0;; ++j) {
@@ -521,9 +529,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           if (lane == 0) trace_ev(tr, 4, n);
           tc_fence_after();
           const uint64_t db = dPS0 + uint64_t(((n % NPB) * C::kPBStride) >> 4);
-#pragma unroll
-          for (int s = 0; s < 8; ++s)
-            umma_bf16_warp_off(tV, da, uint32_t(s * 128), db, uint32_t(s * 128), idGK, (p > 0 || s > 0) ? 1u : 0u);
+          umma_bf16_run<8, 128, 128>(tV, da, db, idGK, p > 0);
           umma_commit_warp(&sm->g_empty[go]);
           umma_commit_warp(&sm->g_empty[gq]);
         }
@@ -545,9 +551,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             if (p == 0 && acn >= 2) mbar_wait_warp(&sm->acc_free[ab], ((acn >> 1) & 1) ^ 1);  // epilogue of task-2 read it
             named_bar_b(kBarPFull, kCompute + 32);
             tc_fence_after();
-#pragma unroll
-            for (int s = 0; s < 8; ++s)
-              umma_bf16_warp_off(tV, da, uint32_t(s * 128), dP0, uint32_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+            umma_bf16_run<8, 128, 128>(tV, da, dP0, idG, p > 0);
             umma_commit_warp(&sm->g_empty[g]);
           }
           if (p + 1 < npairs) {
@@ -560,9 +564,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             const uint64_t da = make_sdesc_sw128(aG + goff, (D == 128) ? lboZ : lboZ - goff, 1024);
             named_bar_b(kBarDsFull, kCompute + 32);
             tc_fence_after();
-#pragma unroll
-            for (int s = 0; s < 8; ++s)
-              umma_bf16_warp_off(tK, da, uint32_t(s * 128), dS0, uint32_t(s * 128), idG, (p > 0 || s > 0) ? 1u : 0u);
+            umma_bf16_run<8, 128, 128>(tK, da, dS0, idG, p > 0);
             umma_commit_warp(&sm->g_empty[g]);
           }
         }

@@ -323,10 +323,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         named_bar(kFbPFull + (gp & 1), 288);                  // P^T(gp) written
         if (p == 0 && j >= 2) named_bar(kFbOFree + tb, 160);  // O^T[tb] read by the epilogue of cube j-2
         tc_fence_after();
-#pragma unroll
-        for (int s = 0; s < 8; ++s)
-          umma_bf16_warp_off(tbase + 128 + tb * 64, a0, uint32_t(s * 128), b0, uint32_t(s * 128), idO,
-                             (p > 0 || s > 0) ? 1u : 0u);
+        umma_bf16_run<8, 128, 128>(tbase + 128 + tb * 64, a0, b0, idO, p > 0);
         umma_commit_warp(&sm->g_empty[g]);
         umma_commit_warp(&sm->o_done[gp & 1]);
         if (p == np - 1) umma_commit_warp(&sm->o_full[tb]);
