@@ -10,8 +10,16 @@
 // pooled values (and everything the coarse stage derives from them) are
 // bit-exact with the oracle. HBM-bound: algorithmic bytes per tensor =
 // read bh*seq*d*es + write bh*seqp*d*es + write bh*nc*d*4.
+#include <algorithm>
+#include <type_traits>
+
 #include "common.cuh"
 #include "launch.h"
+#include "tmap.h"
+
+#ifndef VSA_TILE_TMA
+#define VSA_TILE_TMA 1
+#endif
 
 namespace vsa_dev {
 
@@ -127,6 +135,96 @@ __global__ void __launch_bounds__(128) tile_pool_kernel(DevLayout L, int64_t bh,
   }
 }
 
+// TMA form of K1+K2 for the common case (bf16, [B,H,S,d] raster input, zero / no pad, mean
+// pool, d = 64 or 128): one 5-D tensor-map box per cube (d x cw x ch x ct x 1 unit) lands the
+// cube in shared memory already in tile order -- rows outside the valid raster read as zeros,
+// which IS the zero-pad extension -- and one 1-D bulk copy stores it to the tiled tensor.
+// The pool reads the staged cube: thread i sums channel i over the cube's tokens in tile order
+// (the oracle's order, bit-exact). Persistent CTAs walk the cubes of the three tensors with
+// kTpStages cubes in flight; no thread touches the streamed bytes in registers except the pool.
+#ifndef VSA_TP_STAGES
+#define VSA_TP_STAGES 6
+#endif
+#ifndef VSA_TP_PER_SM
+#define VSA_TP_PER_SM 2
+#endif
+constexpr int kTpStages = VSA_TP_STAGES;
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0, int32_t c1,
+                                            int32_t c2, int32_t c3, int32_t c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<uint64_t>(dst)),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) tile_pool_tma_kernel(const __grid_constant__ CUtensorMap m0,
+                                                            const __grid_constant__ CUtensorMap m1,
+                                                            const __grid_constant__ CUtensorMap m2, DevLayout L,
+                                                            int64_t bh, int n, TilePoolArgs<__nv_bfloat16> a) {
+  extern __shared__ __align__(128) uint8_t tp_smem[];
+  __shared__ uint64_t full[kTpStages];
+  const uint32_t bytes = uint32_t(L.cube) * D * 2;
+  const int64_t per = bh * L.nc, total = per * n;
+  const int tid = int(threadIdx.x);
+  const int64_t g0 = blockIdx.x, step = gridDim.x;
+  const int plane = L.nh * L.nw;
+  auto load = [&](int64_t j) {  // thread 0: cube item j of this CTA into stage j % kTpStages
+    const int64_t g = g0 + j * step;
+    if (g >= total) return;
+    const int tsr = int(g / per);
+    const int64_t r = g - int64_t(tsr) * per, u = r / L.nc;
+    const int c = int(r - u * L.nc);
+    const int ci = c / plane, rem = c - ci * plane, cj = rem / L.nw, ck = rem - cj * L.nw;
+    const int st = int(j % kTpStages);
+    mbar_arrive_expect_tx(&full[st], bytes);
+    tma_load_5d(tp_smem + st * bytes, tsr == 0 ? &m0 : tsr == 1 ? &m1 : &m2, &full[st], 0, ck * L.cw, cj * L.ch,
+                ci * L.ct, int(u));
+  };
+  if (tid == 0) {
+    for (int i = 0; i < kTpStages; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&m0);
+    if (n > 1) tma_prefetch_desc(&m1);
+    if (n > 2) tma_prefetch_desc(&m2);
+    for (int j = 0; j < kTpStages - 1; ++j) load(j);
+  }
+  __syncthreads();
+  for (int64_t j = 0;; ++j) {
+    const int64_t g = g0 + j * step;
+    if (g >= total) break;
+    const int tsr = int(g / per);
+    const int64_t r = g - int64_t(tsr) * per, u = r / L.nc;
+    const int c = int(r - u * L.nc);
+    const int st = int(j % kTpStages);
+    const uint8_t* cube = tp_smem + st * bytes;
+    mbar_wait(&full[st], uint32_t(j / kTpStages) & 1u);
+    if (tid == 0) {
+      __nv_bfloat16* xt = tsr == 0 ? a.xt[0] : tsr == 1 ? a.xt[1] : a.xt[2];
+      bulk_store(xt + (u * L.seqp + int64_t(c) * L.cube) * D, cube, bytes);
+      bulk_commit_group();
+      bulk_wait_group_read1();  // the store of item j-1 has read its stage: reload it
+      load(j + kTpStages - 1);
+    }
+    if (tid < D) {  // the pool: channel tid over the cube's tokens, in tile order
+      const __nv_bfloat16* col = reinterpret_cast<const __nv_bfloat16*>(cube) + tid;
+      float acc = 0.f;
+      for (int o = 0; o < L.cube; ++o) acc = acc + __bfloat162float(col[o * D]);
+      float* pooled = tsr == 0 ? a.pooled[0] : tsr == 1 ? a.pooled[1] : a.pooled[2];
+      pooled[(u * L.nc + c) * D + tid] = acc / float(L.cube);
+    }
+    __syncthreads();  // every thread has pooled item j before its stage is reloaded (item j + stages)
+  }
+  if (tid == 0) bulk_wait_group0();
+}
+
 // untile: tiled -> raster row copy, padded rows dropped. One thread per 16 B chunk.
 template <typename T>
 __global__ void untile_kernel(DevLayout L, int64_t bh, int d, const T* __restrict__ xt, T* __restrict__ x) {
@@ -149,6 +247,47 @@ __global__ void untile_kernel(DevLayout L, int64_t bh, int d, const T* __restric
 namespace vsa_host {
 using namespace vsa_dev;
 
+// The TMA form when its case holds (see tile_pool_tma_kernel); returns false to fall back.
+static bool launch_tile_pool_tma(const vsa_layout_t& Lh, int64_t bh, int64_t d, int32_t n,
+                                 const TilePoolArgs<__nv_bfloat16>& a, int32_t pool_mode, int in_tiled,
+                                 cudaStream_t st) {
+  if (!VSA_TILE_TMA || in_tiled || pool_mode != VSA_POOL_MEAN || Lh.pad_mode == VSA_PAD_MASK || Lh.io_order != 0 ||
+      (d != 64 && d != 128) || n < 1 || n > 3 || Lh.cube > 64 || Lh.ct > 256 || Lh.ch > 256 || Lh.cw > 256)
+    return false;
+  CUtensorMap maps[3];
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) return false;
+  for (int i = 0; i < n; ++i) {
+    if (!a.xt[i] || !a.pooled[i] || (reinterpret_cast<uintptr_t>(a.x[i]) | reinterpret_cast<uintptr_t>(a.xt[i])) % 16)
+      return false;
+    cuuint64_t dims[5] = {cuuint64_t(d), cuuint64_t(Lh.w), cuuint64_t(Lh.h), cuuint64_t(Lh.t), cuuint64_t(bh)};
+    cuuint64_t strides[4] = {cuuint64_t(d) * 2, cuuint64_t(Lh.w) * d * 2, cuuint64_t(Lh.h) * Lh.w * d * 2,
+                             cuuint64_t(Lh.t) * Lh.h * Lh.w * d * 2};
+    cuuint32_t box[5] = {cuuint32_t(d), cuuint32_t(Lh.cw), cuuint32_t(Lh.ch), cuuint32_t(Lh.ct), 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    if (fn(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<__nv_bfloat16*>(a.x[i]), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  for (int i = n; i < 3; ++i) maps[i] = maps[0];
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int smem = kTpStages * int(Lh.cube * d * 2);
+  const int64_t items = bh * Lh.nc * n;
+  const int per_sm = d == 64 ? 2 * VSA_TP_PER_SM : VSA_TP_PER_SM;
+  const int grid = int(std::min<int64_t>(items, int64_t(sms) * per_sm));
+  if (d == 64) {
+    cudaFuncSetAttribute(tile_pool_tma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    tile_pool_tma_kernel<64><<<grid, 128, smem, st>>>(maps[0], maps[1], maps[2], to_dev(Lh), bh, n, a);
+  } else {
+    cudaFuncSetAttribute(tile_pool_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    tile_pool_tma_kernel<128><<<grid, 128, smem, st>>>(maps[0], maps[1], maps[2], to_dev(Lh), bh, n, a);
+  }
+  return true;
+}
+
 template <typename T>
 static int launch_tile_pool_t(const vsa_layout_t& Lh, int64_t bh, int64_t d, int32_t n, const void* const* xr,
                               void* const* xt, float* const* pooled, int32_t pool_mode, int in_tiled,
@@ -158,6 +297,11 @@ static int launch_tile_pool_t(const vsa_layout_t& Lh, int64_t bh, int64_t d, int
     a.x[i] = static_cast<const T*>(xr[i]);
     a.xt[i] = xt ? static_cast<T*>(xt[i]) : nullptr;
     a.pooled[i] = pooled ? pooled[i] : nullptr;
+  }
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (launch_tile_pool_tma(Lh, bh, d, n, a, pool_mode, in_tiled, st)) {
+      VSA_LAUNCH_CHECK("tile_pool_tma_kernel");
+    }
   }
   const int V = Vec<T>::N;
   const int chunks = int(d) / V;
