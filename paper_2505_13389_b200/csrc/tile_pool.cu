@@ -11,6 +11,7 @@
 // bit-exact with the oracle. HBM-bound: algorithmic bytes per tensor =
 // read bh*seq*d*es + write bh*seqp*d*es + write bh*nc*d*4.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -251,6 +252,9 @@ using namespace vsa_dev;
 static bool launch_tile_pool_tma(const vsa_layout_t& Lh, int64_t bh, int64_t d, int32_t n,
                                  const TilePoolArgs<__nv_bfloat16>& a, int32_t pool_mode, int in_tiled,
                                  cudaStream_t st) {
+  // VSA_HBM_TMA=0 forces the thread-load kernel (tests compare the two bitwise)
+  if (const char* e = std::getenv("VSA_HBM_TMA"))
+    if (e[0] == '0') return false;
   if (!VSA_TILE_TMA || in_tiled || pool_mode != VSA_POOL_MEAN || Lh.pad_mode == VSA_PAD_MASK || Lh.io_order != 0 ||
       (d != 64 && d != 128) || n < 1 || n > 3 || Lh.cube > 64 || Lh.ct > 256 || Lh.ch > 256 || Lh.cw > 256)
     return false;
