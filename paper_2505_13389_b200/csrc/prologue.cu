@@ -120,6 +120,10 @@ __global__ void __launch_bounds__(128) prologue_kernel(DevLayout L, int64_t bh, 
 #define VSA_PRO_PER_SM 4
 #endif
 constexpr int kProStages = VSA_PRO_STAGES;
+#ifndef VSA_PRO_THREADS
+#define VSA_PRO_THREADS 128
+#endif
+constexpr int kProThreads = VSA_PRO_THREADS;
 
 __device__ __forceinline__ void tma_load_5d_p(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0, int32_t c1,
                                               int32_t c2, int32_t c3, int32_t c4) {
@@ -152,7 +156,7 @@ struct ProTmaMaps {
 // SM (the copy rate needs the concurrency); dOc carries its per-channel sum across the slabs
 // of a cube in tile order.
 template <int D>
-__global__ void __launch_bounds__(128) prologue_tma_kernel(const __grid_constant__ ProTmaMaps m, DevLayout L, int64_t bh,
+__global__ void __launch_bounds__(kProThreads) prologue_tma_kernel(const __grid_constant__ ProTmaMaps m, DevLayout L, int64_t bh,
                                                            const float* __restrict__ oc,
                                                            const __nv_bfloat16* __restrict__ of, int adaptation,
                                                            __nv_bfloat16* __restrict__ dof, float* __restrict__ delta,
@@ -202,7 +206,7 @@ __global__ void __launch_bounds__(128) prologue_tma_kernel(const __grid_constant
     for (int j = 0; j < kProStages - 1; ++j) load(j);
   }
   __syncthreads();
-  const int ch = tid % CH;  // this thread's channel chunk (constant: 128 % CH == 0)
+  const int ch = tid % CH;  // this thread's channel chunk (constant: the thread count is a multiple of CH)
   float acc = 0.f;          // dOc of channel tid, carried across the two halves
   (void)total;
   for (int64_t j = 0;; ++j) {
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(128) prologue_tma_kernel(const __grid_constant
     for (int i = 0; i < V; ++i) ocv[i] = oc[(u * L.nc + c) * D + ch * V + i];
     __syncthreads();  // dOc has read Gc before it is overwritten with dGc
     const int64_t trow0 = u * L.seqp + int64_t(c) * L.cube + hf * half;
-    for (int k = tid; k < half * CH; k += 128) {
+    for (int k = tid; k < half * CH; k += kProThreads) {
       const int o = k / CH;
       const int off = o * D + ch * V;
       float g_o[V], g_c[V], g_f[V], f_o[V], r_f[V];
@@ -325,11 +329,11 @@ static bool launch_prologue_tma(const vsa_layout_t& Lh, int64_t bh, int64_t d, i
   const DevLayout L = to_dev(Lh);
   if (d == 64) {
     cudaFuncSetAttribute(prologue_tma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    prologue_tma_kernel<64><<<grid, 128, smem, st>>>(m, L, bh, oc, static_cast<const T*>(of), adaptation,
+    prologue_tma_kernel<64><<<grid, kProThreads, smem, st>>>(m, L, bh, oc, static_cast<const T*>(of), adaptation,
                                                      static_cast<T*>(dof), delta, doc, dgc != nullptr, dgf != nullptr, parts);
   } else {
     cudaFuncSetAttribute(prologue_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    prologue_tma_kernel<128><<<grid, 128, smem, st>>>(m, L, bh, oc, static_cast<const T*>(of), adaptation,
+    prologue_tma_kernel<128><<<grid, kProThreads, smem, st>>>(m, L, bh, oc, static_cast<const T*>(of), adaptation,
                                                       static_cast<T*>(dof), delta, doc, dgc != nullptr, dgf != nullptr, parts);
   }
   return true;
