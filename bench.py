@@ -419,13 +419,18 @@ def run_ours(args, rank, world, local_rank):
                                "frac": round(l2_bytes[s] / (max(stage_ms[s], 1e-9) * 1e-3) / 1e9 / l2_peak, 4)}
                            for s in ("fine_fwd", "fine_bwd")}}
     bytes_tp = n * 3 * (S * d * 2 + L.seq_padded * d * 2 + nc * d * 4)  # K1 runs on whole units
+    # K6a: reads dO, Gc, Gf (raster) + the tiled fine output + Oc cubes; writes dOf (tiled),
+    # dGc, dGf (raster), delta (fp32 per tiled row) and the dOc cube sums
+    bytes_pro = n * (5 * S * d * 2 + 2 * L.seq_padded * d * 2 + L.seq_padded * 4 + 2 * nc * d * 4)
+    hbm_bytes = {"tile_pool": bytes_tp, "prologue": bytes_pro}
     stages = {}
     for s in STAGES:
         e = {"ms": round(stage_ms[s], 4)}
         if s in ("fine_fwd", "fine_bwd", "coarse_fwd", "coarse_bwd") and stage_ms[s] > 0:
             e["tflops"] = round(fl_r[s] / (stage_ms[s] * 1e-3) / 1e12, 1)
-        if s == "tile_pool" and stage_ms[s] > 0:
-            e["gbs"] = round(bytes_tp / (stage_ms[s] * 1e-3) / 1e9, 1)
+        if s in hbm_bytes and stage_ms[s] > 0:  # HBM passes: algorithmic bytes / time vs the copy rate
+            e["gbs"] = round(hbm_bytes[s] / (stage_ms[s] * 1e-3) / 1e9, 1)
+            e["frac_of_copy"] = round(e["gbs"] / peaks["hbm"], 3)
         stages[s] = e
     line = {
         "metric": metric_name(cfg),
